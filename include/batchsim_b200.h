@@ -81,6 +81,138 @@ int bs_pose_to_matrix_f64(const double* p, const double* q, int64_t n, double* m
 int bs_pose_from_matrix_f64(const double* m, int64_t n, double* p_out, double* q_out,
                             double* err_out, void* stream);
 
+/* ------------------------------------------------------ scene store (SoA) ---- */
+/* The SoA GPU state store that replaces the reference's per-env SceneBatch objects
+ * (SPEC.md:168-236).  Tables describe each DISTINCT env layout ("model"); envs point at a
+ * model by index, so a homogeneous batch stores one copy.  All arrays are row-major with
+ * the fixed strides given by the *_max fields.  Field order is part of the ABI. */
+
+enum { BS_KIND_SPHERE = 0, BS_KIND_BOX = 1, BS_KIND_CAPSULE = 2, BS_KIND_CYLINDER = 3,
+       BS_KIND_PLANE = 4 };
+enum { BS_JOINT_FIXED = 0, BS_JOINT_REVOLUTE = 1, BS_JOINT_PRISMATIC = 2 };
+enum { BS_BODY_LINK = 0, BS_BODY_ACTOR = 1, BS_BODY_STATIC = 2 };
+/* pair routine codes (bit 4 = roles swapped); 0 = unsupported pair (counted) */
+enum { BS_PAIR_UNSUPPORTED = 0, BS_PAIR_SPHERE_PLANE = 1, BS_PAIR_BOX_PLANE = 2,
+       BS_PAIR_SPHERE_SPHERE = 3, BS_PAIR_SPHERE_BOX = 4, BS_PAIR_CAPSULE_PLANE = 5,
+       BS_PAIR_SWAP = 16 };
+enum { BS_CTRL_PD_JOINT_POS = 0, BS_CTRL_PD_JOINT_DELTA_POS = 1, BS_CTRL_PD_EE_DELTA_POSE = 2 };
+enum { BS_TASK_NONE = 0, BS_TASK_PICKCUBE = 1, BS_TASK_OPENCHAIN = 2 };
+
+typedef struct BsModelTables {
+  int32_t num_models, L_max, D_max, S_max, P_max, A_max, C_max;
+  const int32_t* n_links;      /* [M] */
+  const int32_t* n_dof;        /* [M] */
+  const int32_t* n_shapes;     /* [M] */
+  const int32_t* n_pairs;      /* [M] */
+  const int32_t* n_actors;     /* [M] */
+  const int32_t* link_parent;  /* [M][L_max]  -1 = root attached to the world */
+  const int32_t* link_jtype;   /* [M][L_max]  BS_JOINT_* (roots: FIXED)         */
+  const int32_t* link_dof;     /* [M][L_max]  dof index or -1                   */
+  const int32_t* link_grounded;/* [M][L_max]  1 = no movable joint to the world */
+  const double* link_axis;     /* [M][L_max][3] joint axis (child frame)        */
+  const double* link_org;      /* [M][L_max][7] joint origin (roots: base pose) p,q */
+  const double* link_mass;     /* [M][L_max]                                     */
+  const double* link_com;      /* [M][L_max][3] COM in the link frame            */
+  const double* link_inertia;  /* [M][L_max][6] about COM, link axes: xx yy zz xy xz yz */
+  const double* dof_lower;     /* [M][D_max] */
+  const double* dof_upper;     /* [M][D_max] */
+  const double* dof_damping;   /* [M][D_max] */
+  const double* dof_kp;        /* [M][D_max] drive stiffness (0 = undriven)     */
+  const double* dof_kd;        /* [M][D_max] */
+  const double* dof_flim;      /* [M][D_max] force limit (inf allowed)          */
+  const int32_t* dof_ctrl;     /* [M][D_max] controller action index or -1      */
+  const int32_t* shape_btype;  /* [M][S_max] BS_BODY_*                          */
+  const int32_t* shape_body;   /* [M][S_max] link / actor / static index       */
+  const int32_t* shape_kind;   /* [M][S_max] BS_KIND_*                          */
+  const int32_t* shape_seg;    /* [M][S_max] segmentation id (1 + entity slot)  */
+  const double* shape_size;    /* [M][S_max][3] */
+  const double* shape_frame;   /* [M][S_max][7] local pose (statics: world pose) */
+  const double* shape_radius;  /* [M][S_max] bounding radius (plane: inf)       */
+  const float* shape_color;    /* [M][S_max][4] base RGBA                        */
+  const int32_t* pair_i;       /* [M][P_max] first shape slot (body A)           */
+  const int32_t* pair_j;       /* [M][P_max] second shape slot (body B)          */
+  const int32_t* pair_code;    /* [M][P_max] BS_PAIR_* (| BS_PAIR_SWAP)          */
+  const double* actor_mass;    /* [M][A_max] */
+  const double* actor_inertia; /* [M][A_max][3] principal, body frame            */
+} BsModelTables;
+
+typedef struct BsEnvState {
+  int32_t num_envs;
+  int64_t env_offset;          /* global index of env 0 on this shard (RNG key)  */
+  const int32_t* model_id;     /* [N] */
+  double* qpos;                /* [N][D_max] */
+  double* qvel;                /* [N][D_max] */
+  double* target;              /* [N][D_max] last drive targets                  */
+  double* actor_pose;          /* [N][A_max][7] p, q                             */
+  double* actor_vel;           /* [N][A_max][6] v, w (world)                     */
+  double* link_pose;           /* [N][L_max][7] FK cache after the step          */
+  double* goal;                /* [N][3] task goal                               */
+  uint8_t* diverged;           /* [N] sticky until reset                         */
+  int32_t* elapsed;            /* [N] steps in the current episode               */
+  uint32_t* reset_count;       /* [N] episodes started (RNG counter)             */
+  int32_t* target_dof;         /* [N] task-designated dof (OpenChain) or -1      */
+} BsEnvState;
+
+typedef struct BsStepOutputs {
+  float* obs;                  /* [N][obs_dim] state observation (may be NULL)   */
+  int32_t obs_dim;
+  float* reward;               /* [N] */
+  uint8_t* terminated;         /* [N] */
+  uint8_t* truncated;          /* [N] */
+  uint8_t* success;            /* [N] raw success this step (info)               */
+  uint8_t* fail;               /* [N] */
+  int32_t* unsupported_pairs;  /* [N] broadphase hits of unsupported pair types  */
+  int32_t* contact_count;      /* [N] contacts in the last substep (may be NULL) */
+  int32_t* contact_pairs;      /* [N][C_max][2] shape slots (may be NULL)        */
+  double* contact_geom;        /* [N][C_max][7] point, normal, depth (may be NULL) */
+} BsStepOutputs;
+
+typedef struct BsSimParams {
+  double dt;                   /* 1 / sim_freq                                   */
+  int32_t substeps;            /* sim_freq / control_freq                        */
+  int32_t pos_iters, vel_iters;
+  double gravity[3];
+  double friction, beta, slop;
+  int32_t ctrl_mode;           /* BS_CTRL_*                                      */
+  int32_t action_dim;
+  double action_scale;
+  double ik_lambda;
+  int32_t ee_link;             /* controller / task end-effector link index      */
+  int32_t task;                /* BS_TASK_*                                      */
+  int32_t max_steps;           /* time limit T                                   */
+  int32_t auto_reset;          /* 1: reset terminated|truncated envs in-kernel   */
+  int32_t early_termination;   /* 1: terminated = success | fail                 */
+  uint64_t seed;
+  double task_f[16];           /* task constants (documented per task in DESIGN.md) */
+} BsSimParams;
+
+/* One control step for every env: controller -> substeps x (drives + dynamics +
+ * contacts + PGS + integration + limits + divergence) -> FK cache -> task evaluation ->
+ * state obs -> in-kernel auto-reset.  Replaces env.step over
+ * dynamics.step and controllers.apply.
+ * action: [N][action_dim] float32 in [-1, 1] (clipped). */
+int bs_step(const BsModelTables* tables, const BsEnvState* state, const BsStepOutputs* out,
+            const BsSimParams* params, const float* action, void* stream);
+
+/* Reset the envs selected by env_mask ([N] uint8, NULL = all) from their Philox streams,
+ * then refresh the FK cache and the state obs.  Replaces env.reset. */
+int bs_reset(const BsModelTables* tables, const BsEnvState* state, const BsStepOutputs* out,
+             const BsSimParams* params, const uint8_t* env_mask, int32_t bump_count,
+             void* stream);
+
+/* Forward kinematics of the current qpos into state->link_pose. */
+int bs_forward_kinematics(const BsModelTables* tables, const BsEnvState* state, void* stream);
+
+/* Random actions in [-1,1) (Philox, counter = (blk, step, global env, 'ACT!')) --
+ * the benchmark's "1000 random actions" generated on the device. */
+int bs_random_actions(uint64_t seed, int64_t step, int64_t env_offset, int32_t num_envs,
+                      int32_t action_dim, float* action_out, void* stream);
+
+/* Masked state copy for set_state(snapshot, env_mask): for every env
+ * with mask != 0 copy `row_bytes` bytes of row e from src to dst. */
+int bs_masked_copy(const void* src, void* dst, int64_t num_envs, int64_t row_bytes,
+                   const uint8_t* env_mask, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

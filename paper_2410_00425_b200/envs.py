@@ -1,0 +1,210 @@
+"""Vectorised environment protocol over the device scene store.
+
+``Env.step(action)`` is one fused kernel launch (``bs_step``: controller -> substeps ->
+FK -> task evaluation -> state obs -> in-kernel auto-reset), followed by one render launch
+when the obs mode has cameras.  With ``use_graph=True`` the whole sequence is captured
+once into a CUDA graph and replayed, so a step costs one graph launch of host time.
+
+Results are device tensors; nothing is copied to the host unless the caller asks.  With
+graphs enabled the returned tensors are the env's static output buffers (overwritten by
+the next step) -- clone them to keep a history.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import NamedTuple
+
+import torch
+
+from . import _native as nat
+from . import cabi
+from .errors import DimensionError, InputError
+
+
+@dataclass
+class SimConfig:
+    """SPEC.md:306 with the Appendix-B names; defaults = the paper's benchmark setup
+    (PAPER.md:386-394): sim 120 Hz, control 60 Hz, 4 position / 0 velocity iterations."""
+
+    sim_freq: int = 120
+    control_freq: int = 60
+    solver_pos_iters: int = 4
+    solver_vel_iters: int = 0
+    gravity: tuple = (0.0, 0.0, -9.81)
+    friction_coeff: float = 1.0
+    restitution: float = 0.0
+    penetration_slop: float = 5e-4
+    baumgarte_beta: float = 0.2
+
+    def __post_init__(self):
+        if self.sim_freq % self.control_freq:
+            raise ValueError("sim_freq must be divisible by control_freq")
+        if self.solver_pos_iters < 0 or self.solver_vel_iters < 0:
+            raise ValueError("solver iterations must be >= 0")
+
+
+class StepResult(NamedTuple):
+    obs: object
+    reward: torch.Tensor
+    terminated: torch.Tensor
+    truncated: torch.Tensor
+    info: dict
+
+
+class Env:
+    """N parallel envs of one task on one GPU (one shard of a multi-GPU batch)."""
+
+    def __init__(self, scene, task: int, task_f, ee_link: int, max_steps: int, seed: int,
+                 sim: SimConfig = None, obs_mode: str = "state", renderer=None, auto_reset: bool = True,
+                 early_termination: bool = True, validate_actions: bool = True, name: str = "task"):
+        self.scene = scene
+        self.name = name
+        self.sim = sim or SimConfig()
+        self.num_envs = scene.num_envs
+        self.device = scene.device
+        self.obs_mode = obs_mode
+        self.renderer = renderer
+        self.validate_actions = validate_actions
+        self.action_dim = scene.action_dim
+        self.seed = int(seed)
+        ctl = scene.control
+        p = cabi.BsSimParams()
+        p.dt = 1.0 / self.sim.sim_freq
+        p.substeps = self.sim.sim_freq // self.sim.control_freq
+        p.pos_iters, p.vel_iters = self.sim.solver_pos_iters, self.sim.solver_vel_iters
+        for i in range(3):
+            p.gravity[i] = self.sim.gravity[i]
+        p.friction, p.beta, p.slop = self.sim.friction_coeff, self.sim.baumgarte_beta, self.sim.penetration_slop
+        p.ctrl_mode = cabi.CTRL[ctl.mode]
+        p.action_dim = self.action_dim
+        p.action_scale, p.ik_lambda = ctl.action_scale, ctl.ik_lambda
+        p.ee_link, p.task, p.max_steps = ee_link, task, max_steps
+        p.auto_reset, p.early_termination = int(auto_reset), int(early_termination)
+        p.seed = self.seed & 0xFFFFFFFFFFFFFFFF
+        for i, v in enumerate(task_f):
+            p.task_f[i] = v
+        self.c_params = p
+        N, dev = self.num_envs, self.device
+        self.obs_dim = 2 * scene.D_max + 3 + 13 * scene.A_max + 3
+        self.state_obs = torch.zeros((N, self.obs_dim), dtype=torch.float32, device=dev)
+        self.reward = torch.zeros(N, dtype=torch.float32, device=dev)
+        self.terminated = torch.zeros(N, dtype=torch.uint8, device=dev)
+        self.truncated = torch.zeros(N, dtype=torch.uint8, device=dev)
+        self.success = torch.zeros(N, dtype=torch.uint8, device=dev)
+        self.fail = torch.zeros(N, dtype=torch.uint8, device=dev)
+        self.unsupported = torch.zeros(N, dtype=torch.int32, device=dev)
+        self.contact_count = torch.zeros(N, dtype=torch.int32, device=dev)
+        self.contact_pairs = torch.zeros((N, scene.C_max, 2), dtype=torch.int32, device=dev)
+        self.contact_geom = torch.zeros((N, scene.C_max, 7), dtype=torch.float64, device=dev)
+        self.action_buf = torch.zeros((N, max(1, self.action_dim)), dtype=torch.float32, device=dev)
+        o = cabi.BsStepOutputs()
+        o.obs, o.obs_dim = self.state_obs.data_ptr(), self.obs_dim
+        for k, t in (("reward", self.reward), ("terminated", self.terminated), ("truncated", self.truncated),
+                     ("success", self.success), ("fail", self.fail), ("unsupported_pairs", self.unsupported),
+                     ("contact_count", self.contact_count), ("contact_pairs", self.contact_pairs),
+                     ("contact_geom", self.contact_geom)):
+            setattr(o, k, t.data_ptr())
+        self.c_out = o
+        self._graph = None
+        self._graph_stream = None
+
+    # ------------------------------------------------------------------ spaces
+    @property
+    def action_space(self):
+        """Box [-1, 1]^D_c."""
+        lo = -torch.ones(self.action_dim)
+        return {"low": lo, "high": -lo, "shape": (self.action_dim,)}
+
+    # ------------------------------------------------------------------ protocol
+    def reset(self, seed=None, env_mask=None):
+        """Re-initialise the selected envs from their RNG streams.
+        A new `seed` re-keys every env's stream; the mask selects a partial reset."""
+        if seed is not None:
+            self.seed = int(seed)
+            self.c_params.seed = self.seed & 0xFFFFFFFFFFFFFFFF
+            self.scene.reset_count.zero_()
+            bump = 0
+        else:
+            bump = 1 if env_mask is not None else 0
+        mask = None
+        if env_mask is not None:
+            mask = torch.as_tensor(env_mask, device=self.device).to(torch.uint8).contiguous()
+            if mask.shape != (self.num_envs,):
+                raise DimensionError(f"env_mask must have shape ({self.num_envs},)")
+        nat.call("bs_reset", ctypes.byref(self.scene.c_tables), ctypes.byref(self.scene.c_state),
+                 ctypes.byref(self.c_out), ctypes.byref(self.c_params),
+                 None if mask is None else mask.data_ptr(), bump, nat.stream_handle())
+        self._render()
+        return self._obs()
+
+    def _launch_step(self, action_ptr):
+        nat.call("bs_step", ctypes.byref(self.scene.c_tables), ctypes.byref(self.scene.c_state),
+                 ctypes.byref(self.c_out), ctypes.byref(self.c_params), action_ptr, nat.stream_handle())
+        self._render()
+
+    def _render(self):
+        if self.renderer is not None:
+            self.renderer.render(self.scene)
+
+    def step(self, action) -> StepResult:
+        """controller -> dynamics -> task evaluation -> reward."""
+        a = action if isinstance(action, torch.Tensor) else torch.as_tensor(action)
+        a = a.to(device=self.device, dtype=torch.float32)
+        if a.shape != (self.num_envs, self.action_dim):
+            raise DimensionError(f"action must have shape ({self.num_envs}, {self.action_dim}), "
+                                 f"got {tuple(a.shape)}")
+        if self.validate_actions and not bool(torch.isfinite(a).all()):
+            raise InputError("non-finite action")
+        if self._graph is not None:
+            self.action_buf.copy_(a)
+            self._graph.replay()
+        else:
+            a = a.contiguous()
+            self._launch_step(a.data_ptr())
+        return self._result()
+
+    def step_random(self, step_index: int) -> StepResult:
+        """Benchmark helper: Philox random actions generated on the device, then step."""
+        nat.call("bs_random_actions", self.seed, step_index, self.scene.env_offset, self.num_envs,
+                 self.action_dim, self.action_buf.data_ptr(), nat.stream_handle())
+        if self._graph is not None:
+            self._graph.replay()
+        else:
+            self._launch_step(self.action_buf.data_ptr())
+        return self._result()
+
+    def capture_graph(self, warmup: int = 2) -> None:
+        """Capture bs_step (+ render) on the static action buffer into a CUDA graph."""
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        snap = self.scene.get_state()
+        with torch.cuda.stream(s):
+            for _ in range(warmup):
+                self._launch_step(self.action_buf.data_ptr())
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._launch_step(self.action_buf.data_ptr())
+        self.scene.set_state(snap)
+        self._graph = g
+
+    def _obs(self):
+        if self.obs_mode == "state":
+            return self.state_obs
+        out = {"state": self.state_obs}
+        if self.renderer is not None:
+            out.update(self.renderer.observation(self.obs_mode))
+        return out
+
+    def _result(self) -> StepResult:
+        info = {"success": self.success, "fail": self.fail, "unsupported_pairs": self.unsupported,
+                "elapsed": self.scene.elapsed, "diverged": self.scene.diverged,
+                "contact_count": self.contact_count}
+        return StepResult(self._obs(), self.reward, self.terminated, self.truncated, info)
+
+    def contacts(self):
+        """The ContactSet of the last substep: per env a count, shape-slot
+        pairs, and point/normal/depth rows."""
+        return self.contact_count, self.contact_pairs, self.contact_geom

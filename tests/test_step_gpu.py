@@ -1,0 +1,219 @@
+"""GPU fused step vs the CPU oracle on the PickCube-style task (config C1: 16 envs, 200
+steps, fp64).
+
+Bars (BASELINE north star): integer outputs bit-exact (contact pair lists, success/fail/
+terminated/truncated flags, unsupported-pair counters, env indexing, random actions);
+float state within a stated tolerance:
+  * one-step parity from an identical state: |dx| <= 1e-9 (abs, m / rad / m/s);
+  * 200-step free-running trajectory: relative 1e-4 on body/articulation state.
+"""
+
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+N, STEPS, SEED = 16, 200, 7
+
+
+@pytest.fixture(scope="module")
+def pair(cuda):
+    from oracle.tasks import PickCubeOracle
+    from paper_2410_00425_b200.tasks import make_task, pickcube_scene
+
+    env = make_task("PickCube", N, seed=SEED)
+    orc = PickCubeOracle(env.spec, pickcube_scene(env.spec), N, SEED)
+    return env, orc
+
+
+def gpu_snapshot(env):
+    s = env.scene
+    ap = s.actor_pose.cpu().numpy()
+    av = s.actor_vel.cpu().numpy()
+    return {"q": s.qpos.cpu().numpy()[:, :3], "qd": s.qvel.cpu().numpy()[:, :3], "ap": ap[:, :, :3],
+            "aq": ap[:, :, 3:], "av": av[:, :, :3], "aw": av[:, :, 3:], "goal": s.goal.cpu().numpy(),
+            "elapsed": s.elapsed.cpu().numpy()}
+
+
+def compare(a, b, atol, rtol=0.0, what=""):
+    for k in ("q", "qd", "ap", "aq", "av", "aw", "goal"):
+        x, y = np.asarray(a[k], np.float64), np.asarray(b[k], np.float64)
+        err = np.abs(x - y)
+        lim = atol + rtol * np.abs(y)
+        assert (err <= lim).all(), f"{what} {k}: max err {err.max():.3e} at {np.unravel_index(err.argmax(), err.shape)}"
+
+
+def actions(env, step):
+    from oracle.philox import action_uniforms
+
+    got = torch.empty((N, env.action_dim), dtype=torch.float32, device=env.device)
+    from paper_2410_00425_b200 import _native as nat
+
+    nat.call("bs_random_actions", SEED, step, 0, N, env.action_dim, got.data_ptr(), nat.stream_handle())
+    want = action_uniforms(SEED, step, np.arange(N), env.action_dim)
+    assert np.array_equal(got.cpu().numpy().view(np.uint32), want.view(np.uint32)), "Philox actions differ"
+    return got, want
+
+
+def test_reset_matches_oracle(pair):
+    env, orc = pair
+    env.reset(seed=SEED)
+    orc.reset_count[:] = 0
+    orc.reset()
+    g = gpu_snapshot(env)
+    o = orc.snapshot()
+    assert np.array_equal(g["q"], o["q"]), "qpos reset is exact arithmetic"
+    assert np.array_equal(g["ap"], o["ap"]) and np.array_equal(g["goal"], o["goal"])
+    compare(g, o, atol=1e-15, what="reset")
+    obs = env.state_obs.cpu().numpy()
+    oo = orc.obs()
+    assert np.abs(obs - oo).max() <= 1e-6
+
+
+def test_one_step_parity_and_integer_outputs(pair):
+    env, orc = pair
+    env.reset(seed=SEED)
+    orc.reset_count[:] = 0
+    orc.reset()
+    n_contacts = 0
+    for t in range(60):
+        orc.load(gpu_snapshot(env))
+        orc.reset_count[:] = env.scene.reset_count.cpu().numpy().astype(np.uint64)
+        a_gpu, a_np = actions(env, t)
+        r = env.step(a_gpu)
+        _, o_rew, o_term, o_trunc, o_info, final = orc.step(a_np, want_contacts=True)
+        # integer outputs: bit-exact
+        assert np.array_equal(r.info["unsupported_pairs"].cpu().numpy(), o_info["unsupported_pairs"])
+        assert np.array_equal(r.terminated.cpu().numpy().astype(bool), o_term)
+        assert np.array_equal(r.truncated.cpu().numpy().astype(bool), o_trunc)
+        assert np.array_equal(r.info["success"].cpu().numpy().astype(bool), o_info["success"])
+        cnt, pairs, geom = (x.cpu().numpy() for x in env.contacts())
+        for e in range(N):
+            want = [(i, j) for (i, j, P, n, d, v) in o_info["contacts"] if v[e]]
+            got = [tuple(pairs[e, c]) for c in range(cnt[e])]
+            assert got == want, f"step {t} env {e}: contact pairs {got} != {want}"
+            wg = np.array([np.concatenate([P[e], n[e], [d[e]]]) for (i, j, P, n, d, v) in o_info["contacts"] if v[e]])
+            if len(wg):
+                assert np.abs(geom[e, :cnt[e]] - wg).max() < 1e-9
+            n_contacts += cnt[e]
+        assert np.abs(r.reward.cpu().numpy() - o_rew).max() < 1e-5
+        # float state after the step (post auto-reset): tight tolerance
+        compare(gpu_snapshot(env), orc.snapshot(), atol=1e-9, what=f"step {t}")
+    assert n_contacts > 0, "the trajectory never touched anything"
+
+
+def test_trajectory_parity_200_steps(pair):
+    env, orc = pair
+    env.reset(seed=SEED)
+    orc.reset_count[:] = 0
+    orc.reset()
+    worst = 0.0
+    for t in range(STEPS):
+        a_gpu, a_np = actions(env, t)
+        r = env.step(a_gpu)
+        _, o_rew, o_term, o_trunc, o_info, _ = orc.step(a_np)
+        assert np.array_equal(r.terminated.cpu().numpy().astype(bool), o_term), f"step {t}"
+        assert np.array_equal(r.truncated.cpu().numpy().astype(bool), o_trunc), f"step {t}"
+        g, o = gpu_snapshot(env), orc.snapshot()
+        compare(g, o, atol=1e-7, rtol=1e-4, what=f"trajectory step {t}")
+        worst = max(worst, max(np.abs(np.asarray(g[k]) - np.asarray(o[k])).max() for k in ("q", "ap")))
+    print(f"max |dx| over {STEPS} steps: {worst:.3e}")
+
+
+def test_determinism_and_snapshot(pair):
+    env, _ = pair
+    env.reset(seed=3)
+    snap = env.scene.get_state()
+    for t in range(10):
+        env.step_random(t)
+    a = env.scene.get_state()
+    env.scene.set_state(snap)
+    for t in range(10):
+        env.step_random(t)
+    b = env.scene.get_state()
+    for k in env.scene.STATE_FIELDS:
+        assert torch.equal(a[k], b[k]), k
+    # partial set_state: env 1 untouched bitwise
+    mask = torch.zeros(N, dtype=torch.uint8)
+    mask[0] = 1
+    before = env.scene.get_state()
+    env.scene.set_state(snap, env_mask=mask)
+    after = env.scene.get_state()
+    for k in env.scene.STATE_FIELDS:
+        assert torch.equal(after[k][1:], before[k][1:]), k
+        assert torch.equal(after[k][0], snap[k][0]), k
+
+
+def test_cross_env_independence(pair):
+    env, _ = pair
+    env.reset(seed=11)
+    snap = env.scene.get_state()
+    for t in range(20):
+        env.step_random(t)
+    ref = env.scene.get_state()
+    env.scene.set_state(snap)
+    env.scene.qvel[5, 1] += 0.5  # perturb env 5 only
+    for t in range(20):
+        env.step_random(t)
+    got = env.scene.get_state()
+    for k in ("qpos", "qvel", "actor_pose", "actor_vel"):
+        keep = torch.ones(N, dtype=torch.bool)
+        keep[5] = False
+        assert torch.equal(got[k][keep], ref[k][keep]), k
+        assert not torch.equal(got[k][5], ref[k][5]) or k == "actor_vel"
+
+
+def test_shard_equivalence(cuda):
+    """Global env indices key the RNG: two shards == one batch, bitwise."""
+    from paper_2410_00425_b200.tasks import make_task
+
+    full = make_task("PickCube", 8, seed=5)
+    lo = make_task("PickCube", 8, seed=5, shard=(0, 2))
+    hi = make_task("PickCube", 8, seed=5, shard=(1, 2))
+    for t in range(15):
+        full.step_random(t)
+        lo.step_random(t)
+        hi.step_random(t)
+    for k in ("qpos", "qvel", "actor_pose", "actor_vel", "goal"):
+        cat = torch.cat([getattr(lo.scene, k), getattr(hi.scene, k)])
+        assert torch.equal(cat, getattr(full.scene, k)), k
+
+
+def test_graph_replay_matches_eager(cuda):
+    from paper_2410_00425_b200.tasks import make_task
+
+    a = make_task("PickCube", 64, seed=9)
+    b = make_task("PickCube", 64, seed=9)
+    b.capture_graph()
+    for t in range(12):
+        a.step_random(t)
+        b.step_random(t)
+    for k in ("qpos", "qvel", "actor_pose", "actor_vel", "elapsed"):
+        assert torch.equal(getattr(a.scene, k), getattr(b.scene, k)), k
+
+
+def test_nonfinite_action_raises(cuda):
+    from paper_2410_00425_b200.errors import InputError
+    from paper_2410_00425_b200.tasks import make_task
+
+    env = make_task("PickCube", 4, seed=0)
+    a = torch.zeros((4, 3), device=env.device)
+    a[2, 1] = float("nan")
+    with pytest.raises(InputError):
+        env.step(a)
+
+
+def test_divergence_flags_and_freezes_only_that_env(cuda):
+    from paper_2410_00425_b200.tasks import make_task
+
+    env = make_task("PickCube", 4, seed=0, auto_reset=False)
+    env.scene.qvel[2, 0] = float("inf")
+    before = env.scene.get_state()
+    r = env.step(torch.zeros((4, 3), device=env.device))
+    assert env.scene.diverged.cpu().tolist() == [0, 0, 1, 0]
+    assert bool(r.info["fail"][2]) and bool(r.terminated[2])
+    assert torch.equal(env.scene.qpos[2], before["qpos"][2])  # frozen
+    assert torch.isfinite(env.scene.qpos[[0, 1, 3]]).all()
