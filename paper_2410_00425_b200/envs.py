@@ -149,30 +149,52 @@ class Env:
             self.renderer.render(self.scene)
 
     def step(self, action) -> StepResult:
-        """controller -> dynamics -> task evaluation -> reward."""
+        """controller -> dynamics -> task evaluation -> reward.
+
+        `action` may live on the host (numpy / CPU tensor; validated there and copied
+        asynchronously, from pinned memory when the caller provides it) or on the device
+        (validated with one device reduction, which synchronises; pass
+        validate_actions=False to the env to skip it)."""
         a = action if isinstance(action, torch.Tensor) else torch.as_tensor(action)
-        a = a.to(device=self.device, dtype=torch.float32)
         if a.shape != (self.num_envs, self.action_dim):
             raise DimensionError(f"action must have shape ({self.num_envs}, {self.action_dim}), "
                                  f"got {tuple(a.shape)}")
-        if self.validate_actions and not bool(torch.isfinite(a).all()):
-            raise InputError("non-finite action")
-        if self._graph is not None:
+        if self.validate_actions:
+            finite = torch.isfinite(a).all()
+            if not bool(finite):
+                raise InputError("non-finite action")
+        if a.device != self.device or a.dtype != torch.float32 or not a.is_contiguous():
+            self.action_buf.copy_(a, non_blocking=True)
+            ptr = self.action_buf.data_ptr()
+        elif self._graph is not None:
             self.action_buf.copy_(a)
+            ptr = self.action_buf.data_ptr()
+        else:
+            ptr = a.data_ptr()
+        if self._graph is not None:
             self._graph.replay()
         else:
-            a = a.contiguous()
-            self._launch_step(a.data_ptr())
+            self._launch_step(ptr)
         return self._result()
 
-    def step_random(self, step_index: int) -> StepResult:
-        """Benchmark helper: Philox random actions generated on the device, then step."""
+    def random_actions(self, step_index: int) -> torch.Tensor:
+        """Philox uniform actions in [-1, 1) for every env, generated on the device into the
+        static action buffer (the benchmark's random-action stream)."""
         nat.call("bs_random_actions", self.seed, step_index, self.scene.env_offset, self.num_envs,
                  self.action_dim, self.action_buf.data_ptr(), nat.stream_handle())
+        return self.action_buf
+
+    def launch_step(self) -> None:
+        """Enqueue one step on the static action buffer (no validation, no host work)."""
         if self._graph is not None:
             self._graph.replay()
         else:
             self._launch_step(self.action_buf.data_ptr())
+
+    def step_random(self, step_index: int) -> StepResult:
+        """Benchmark helper: Philox random actions generated on the device, then step."""
+        self.random_actions(step_index)
+        self.launch_step()
         return self._result()
 
     def capture_graph(self, warmup: int = 2) -> None:

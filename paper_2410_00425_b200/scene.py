@@ -30,21 +30,8 @@ import torch
 from . import _native as nat
 from . import cabi
 from . import hostmath as hm
-from .descriptors import SceneDesc
+from .descriptors import ControlSpec, SceneDesc  # noqa: F401
 from .errors import DimensionError, LayoutMismatchError, SceneBuildError, ViewLookupError
-
-
-@dataclass(frozen=True)
-class ControlSpec:
-    """Controller preset: which articulation the action drives."""
-
-    mode: str = "pd_joint_delta_pos"
-    robot: str = "arm"
-    action_scale: float = 0.1
-    kp: float = 1000.0
-    kd: float = 2.0 * math.sqrt(1000.0)
-    force_limit: float = 100.0
-    ik_lambda: float = 0.05
 
 
 def _bounding_radius(kind, size):

@@ -11,49 +11,16 @@ Tasks on the hot path (BASELINE.json configs):
 
 from __future__ import annotations
 
-import math
-from dataclasses import dataclass, replace
+from dataclasses import replace
 
 from . import cabi
-from . import fixtures as F
-from .assets import load_urdf
-from .descriptors import GROUND, ActorDesc, ArticulationDesc, SceneDesc
+from .descriptors import PickCubeSpec, SceneDesc, pickcube_desc  # noqa: F401
 from .envs import Env, SimConfig
-from .scene import ControlSpec, build_batch
-
-
-@dataclass(frozen=True)
-class PickCubeSpec:
-    arm_base_p: tuple = (-0.5, 0.0, 0.25)
-    q_rest: tuple = (0.0, -0.3, 1.2)
-    q_noise: float = 0.02
-    cube_half: float = 0.02
-    cube_density: float = 1000.0
-    cube_color: tuple = (0.2, 0.4, 0.9, 1.0)
-    cube_xy: float = 0.1
-    goal_xy: float = 0.1
-    success_dist: float = 0.025
-    fail_z: float = -0.1
-    max_steps: int = 100
-    ee_link: str = "ee"
-    control_mode: str = "pd_joint_delta_pos"
-    action_scale: float = 0.1
-    kp: float = 1000.0
-    kd: float = 2.0 * math.sqrt(1000.0)
-    force_limit: float = 100.0
-
-    def task_f(self):
-        return [self.q_noise, self.cube_half, self.cube_xy, self.goal_xy, self.success_dist, self.fail_z,
-                *self.q_rest]
-
-    def control(self):
-        return ControlSpec(self.control_mode, "arm", self.action_scale, self.kp, self.kd, self.force_limit)
+from .scene import build_batch
 
 
 def pickcube_scene(spec: PickCubeSpec) -> SceneDesc:
-    arm = ArticulationDesc("arm", load_urdf(F.ARM3_URDF), tuple(spec.arm_base_p))
-    cube = ActorDesc("cube", "box", (spec.cube_half,) * 3, spec.cube_density, spec.cube_color)
-    return SceneDesc((arm,), (cube,), (GROUND,))
+    return pickcube_desc(spec)
 
 
 TASKS = {}

@@ -163,7 +163,8 @@ def test_cross_env_independence(pair):
         keep = torch.ones(N, dtype=torch.bool)
         keep[5] = False
         assert torch.equal(got[k][keep], ref[k][keep]), k
-        assert not torch.equal(got[k][5], ref[k][5]) or k == "actor_vel"
+    # the perturbed env itself moved differently (its arm; the cube may be untouched)
+    assert not torch.equal(got["qpos"][5], ref["qpos"][5])
 
 
 def test_shard_equivalence(cuda):
