@@ -213,6 +213,59 @@ int bs_random_actions(uint64_t seed, int64_t step, int64_t env_offset, int32_t n
 int bs_masked_copy(const void* src, void* dst, int64_t num_envs, int64_t row_bytes,
                    const uint8_t* env_mask, void* stream);
 
+
+/* ------------------------------------------------------------- batched rasterizer ---- */
+/* Tessellated shapes of every model (SPEC.md:461 counts: sphere 320, box 12, capsule 512,
+ * cylinder 64 triangles; the ground plane is a finite grid, A-9/A-11).  Vertices
+ * are float32 in the shape's local frame; triangles index model-local vertices and are
+ * wound counter-clockwise around the outward normal. */
+typedef struct BsMeshTables {
+  int32_t num_models, V_max, T_max;
+  const int32_t* n_verts;      /* [M] */
+  const int32_t* n_tris;       /* [M] */
+  const float* verts;          /* [M][V_max][3] */
+  const int32_t* vert_shape;   /* [M][V_max] shape slot of the vertex */
+  const int32_t* tris;         /* [M][T_max][3] */
+  const int32_t* tri_shape;    /* [M][T_max] shape slot of the triangle */
+} BsMeshTables;
+
+/* CameraConfig: one group of cameras sharing a resolution.  OpenCV axes
+ * (x right, y down, z forward); pose = camera -> world, or the local offset on the mount
+ * link when mount_link[c] >= 0 (camera pose = link pose o offset). */
+typedef struct BsCameraBatch {
+  int32_t num_cams, width, height;
+  float near_plane, far_plane;
+  const int32_t* mount_link;   /* [C] link slot or -1 (may be NULL: all world-fixed) */
+  const double* pose;          /* [N][C][7] p, q (w,x,y,z) */
+  const float* intrinsics;     /* [N][C][4] fx, fy, cx, cy (pixels) */
+} BsCameraBatch;
+
+typedef struct BsRenderParams {
+  double light_dir[3];         /* unit vector towards the light, world frame */
+  float ambient, diffuse;      /* flat shading: ambient + diffuse * max(0, n.l) (A-12) */
+  float background[3];         /* rgb in [0,1] of empty pixels */
+  int32_t tile;                /* CTA tile edge in pixels (0 = default 64) */
+} BsRenderParams;
+
+/* FrameBatch + the fused pointcloud (A-10).  Any pointer
+ * may be NULL (that output is skipped).  Layouts: rgb [N][C][H][W][3] u8, depth [N][C][H][W]
+ * f32 (0 = no hit), seg [N][C][H][W] u16 (0 = background), pointcloud [N][C][H*W][6] f32
+ * (world xyz, rgb in [0,1]; all-zero where seg == 0). */
+typedef struct BsFrameBatch {
+  uint8_t* rgb;
+  float* depth;
+  uint16_t* seg;
+  float* pointcloud;
+} BsFrameBatch;
+
+/* render(scene, cameras) + pointcloud for every env and
+ * camera of the group, from the link-pose cache and actor poses in `state`.  env_color:
+ * [N][S_max][3] float per-env shape colours (texture randomisation) or NULL for the model
+ * colours. */
+int bs_render(const BsModelTables* tables, const BsEnvState* state, const BsMeshTables* mesh,
+              const BsCameraBatch* cams, const float* env_color, const BsRenderParams* params,
+              const BsFrameBatch* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -81,7 +81,6 @@ def load():
         raise ImportError(f"{LIB_PATH} has ABI {ver}, expected {ABI_VERSION}; rebuild it")
     _lib = lib
     from . import cabi  # noqa: F401  (registers the struct-taking entry points)
-    from . import render_abi  # noqa: F401
     return lib
 
 

@@ -32,6 +32,7 @@ NOFMA = ["-fmad=false"]
 SOURCES = {
     "pose.cu": NOFMA,
     "sim.cu": [],
+    "step.cu": [],
     "raster.cu": NOFMA,
     "capi.cu": [],
 }

@@ -42,12 +42,36 @@ class BsSimParams(ctypes.Structure):
                 ("early_termination", I32), ("seed", ctypes.c_uint64), ("task_f", F64 * 16)]
 
 
+F32 = ctypes.c_float
+
+
+class BsMeshTables(ctypes.Structure):
+    _fields_ = [("num_models", I32), ("V_max", I32), ("T_max", I32)] + [
+        (n, P) for n in ("n_verts", "n_tris", "verts", "vert_shape", "tris", "tri_shape")]
+
+
+class BsCameraBatch(ctypes.Structure):
+    _fields_ = [("num_cams", I32), ("width", I32), ("height", I32), ("near_plane", F32), ("far_plane", F32),
+                ("mount_link", P), ("pose", P), ("intrinsics", P)]
+
+
+class BsRenderParams(ctypes.Structure):
+    _fields_ = [("light_dir", F64 * 3), ("ambient", F32), ("diffuse", F32), ("background", F32 * 3),
+                ("tile", I32)]
+
+
+class BsFrameBatch(ctypes.Structure):
+    _fields_ = [(n, P) for n in ("rgb", "depth", "seg", "pointcloud")]
+
+
 _R = ctypes.POINTER
 _native.register("bs_step", [_R(BsModelTables), _R(BsEnvState), _R(BsStepOutputs), _R(BsSimParams), P, P])
 _native.register("bs_reset", [_R(BsModelTables), _R(BsEnvState), _R(BsStepOutputs), _R(BsSimParams), P, I32, P])
 _native.register("bs_forward_kinematics", [_R(BsModelTables), _R(BsEnvState), P])
 _native.register("bs_random_actions", [ctypes.c_uint64, I64, I64, I32, I32, P, P])
 _native.register("bs_masked_copy", [P, P, I64, I64, P, P])
+_native.register("bs_render", [_R(BsModelTables), _R(BsEnvState), _R(BsMeshTables), _R(BsCameraBatch), P,
+                               _R(BsRenderParams), _R(BsFrameBatch), P])
 
 # enum values (include/batchsim_b200.h)
 KIND = {"sphere": 0, "box": 1, "capsule": 2, "cylinder": 3, "plane": 4}

@@ -1,0 +1,919 @@
+// Fused control step for every env (bs_step): controller -> substeps (FK, RNEA bias + CRBA
+// mass matrix + implicit PD drives -> Cholesky -> M^-1, free-body gyroscopics, shape poses,
+// broadphase + narrowphase over the static pair list, ordered contact compaction, PGS rows,
+// projected Gauss-Seidel, semi-implicit Euler, joint limits, divergence freeze) -> FK cache
+// -> task evaluation -> state obs -> in-kernel auto-reset.
+//
+// Reference semantics: SPEC.md:319-354 (dynamics), 249-257 (FK), 402-410 (controllers),
+// 536-553 (reset/step), with DESIGN.md's decisions register (A-4..A-25).  The CPU oracle
+// (oracle/engine.py) restates the same algorithm independently; tests/test_step_gpu.py
+// holds the two together.
+//
+// Execution model (v1, B200): G = 8 lanes cooperate on one env, 4 envs per warp, one warp
+// per CTA.  Every env's working set (state, link poses, spatial inertias, RNEA temporaries,
+// M^-1, shape poses, contacts and PGS rows) is staged in shared memory (about 8 KB for the
+// PickCube scene), so 28 envs -- 4096 envs over 148 SMs -- are resident at once.  Work that is
+// parallel inside an env (links, shapes, actors, pairs, contact slots, constraint rows, M^-1
+// columns, obs entries, state rows) is spread over the lanes; the inherently serial parts
+// (FK chain, RNEA passes, Cholesky, the Gauss-Seidel sweep, whose row order is part of the
+// result) run on the group's lanes redundantly or on lane 0, with __syncwarp between phases
+// and ballots/shuffles for the compaction and reductions.  No fp64 division sits in the
+// sweep: rows carry 1/K and M^-1 is explicit (the oracle also forms inv(Mt)).  Nothing in the
+// step is a dense contraction, so there are no tensor cores; the kernel is latency/ALU
+// bound and moves ~0.8 KB of HBM per env-step.
+#include "sim_common.cuh"
+
+namespace bs {
+namespace step {
+
+using namespace bs::sim;
+
+#define FULLMASK 0xffffffffu
+
+// Per-env shared-memory layout, offsets in doubles (computed on the host from the table
+// maxima; identical for every env of the launch).
+struct Lay {
+  int Dm, Lm, Sm, Cm, Am, NU, RW, KCH;
+  int q, qd, tgt, apose, avel, goal;
+  int lpq, Sv, In, Mt, Minv, cb, uq, uv, uw, Iwi, spq;
+  int Tl, V, Ac, F, ct, rows;
+  int total;
+};
+
+// Generalised velocity u (length NU = D_max + 6 A_max): [0, D_max) joint rates, then per actor
+// slot a: linear velocity at [D_max + 6a, +3), angular at [D_max + 6a + 3, +3).
+// Row layout (dense over u): [0] 1/K (0 = skip)  [1] lambda  [2] position-phase target
+// [3] velocity-phase target  [4, 4+NU) J  [4+NU, 4+2NU) W = M_u^-1 J^T (the velocity change per
+// unit impulse).  Rows touch at most two bodies, but a dense row has no per-row branching,
+// no actor-index selects and no int conversions in the sweep.
+#define ROW_J 4
+
+template <int G_, int MD_, int MA_>
+struct Cfg {
+  static constexpr int G = G_, MD = MD_, MA = MA_, EPW = 32 / G_, NU = MD_ + 6 * MA_;
+};
+
+__device__ __forceinline__ R sgn_of(R v) { return v > 0.0 ? 1.0 : -1.0; }
+
+// Unit quaternion with the reference's sign rule (pose.py:31-40) but reciprocal-sqrt
+// scaling (the step is tolerance-gated, not bit-gated).
+__device__ __forceinline__ Q4<R> qnorm_f(Q4<R> q) {
+  R ss = q.w * q.w;
+  ss = ss + q.x * q.x;
+  ss = ss + q.y * q.y;
+  ss = ss + q.z * q.z;
+  R inv = rsqrt(ss);
+  Q4<R> r{q.w * inv, q.x * inv, q.y * inv, q.z * inv};
+  R s = r.w != 0.0 ? sgn_of(r.w) : r.x != 0.0 ? sgn_of(r.x) : r.y != 0.0 ? sgn_of(r.y) : (r.z < 0.0 ? -1.0 : 1.0);
+  return Q4<R>{r.w * s, r.x * s, r.y * s, r.z * s};
+}
+
+__device__ __forceinline__ void compose_f(V3<R> pa, Q4<R> qa, V3<R> pb, Q4<R> qb, V3<R>& po, Q4<R>& qo) {
+  V3<R> r = quat_rotate(qa, pb);
+  po = add(pa, r);
+  qo = qnorm_f(quat_mul(qa, qb));
+}
+
+__device__ __forceinline__ void st7(R* d, V3<R> p, Q4<R> q) {
+  d[0] = p.x; d[1] = p.y; d[2] = p.z; d[3] = q.w; d[4] = q.x; d[5] = q.y; d[6] = q.z;
+}
+__device__ __forceinline__ V6 ld6(const R* s) { return V6{{s[0], s[1], s[2]}, {s[3], s[4], s[5]}}; }
+__device__ __forceinline__ void st6(R* d, const V6& a) {
+  d[0] = a.w[0]; d[1] = a.w[1]; d[2] = a.w[2]; d[3] = a.v[0]; d[4] = a.v[1]; d[5] = a.v[2];
+}
+__device__ __forceinline__ V6 add6(const V6& a, const V6& b) { return mk6(add(gw(a), gw(b)), add(gv(a), gv(b))); }
+__device__ __forceinline__ Inertia ldI(const R* s) {
+  Inertia I;
+  I.m = s[0];
+  I.h = ld3(s + 1);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) I.I[k] = s[4 + k];
+  return I;
+}
+__device__ __forceinline__ void stI(R* d, const Inertia& I) {
+  d[0] = I.m;
+  st3(d + 1, I.h);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) d[4 + k] = I.I[k];
+}
+
+__device__ __forceinline__ int pair_maxc(int code) {
+  switch (code & 15) {
+    case BS_PAIR_SPHERE_PLANE: return 1;
+    case BS_PAIR_BOX_PLANE: return 4;
+    case BS_PAIR_SPHERE_SPHERE: return 1;
+    case BS_PAIR_SPHERE_BOX: return 1;
+    case BS_PAIR_CAPSULE_PLANE: return 2;
+    default: return 0;
+  }
+}
+
+// Actor world inertia and its inverse: R diag(I) R^T, R diag(1/I) R^T (A-8).
+__device__ __forceinline__ void actor_inertia_f(const R* Ib, Q4<R> q, R* Iw, R* Iwi) {
+  R r[9];
+  quat_to_matrix(q, r);
+  R ib[3] = {Ib[0], Ib[1], Ib[2]};
+  R ii[3] = {1.0 / Ib[0], 1.0 / Ib[1], 1.0 / Ib[2]};
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      R s = 0, si = 0;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        s += r[3 * i + k] * ib[k] * r[3 * j + k];
+        si += r[3 * i + k] * ii[k] * r[3 * j + k];
+      }
+      Iw[3 * i + j] = s;
+      Iwi[3 * i + j] = si;
+    }
+}
+
+// A candidate contact slot: [0..3) point (midpoint), [3..6) normal (second -> first body),
+// [6] depth, [7] pair index (-1 = empty slot).
+__device__ __forceinline__ void put_cand(R* c, V3<R> sB, V3<R> n, R depth, int pair, bool flip, R slop) {
+  if (!(depth >= -slop)) { c[7] = -1.0; return; }
+  V3<R> p = sub(sB, scl(n, 0.5 * depth));
+  V3<R> nn = flip ? scl(n, -1.0) : n;
+  st3(c, p);
+  st3(c + 3, nn);
+  c[6] = depth;
+  c[7] = (R)pair;
+}
+
+// Narrowphase of one static pair (A-4, A-25) into its fixed slots.
+// Returns 1 when the pair passed the broadphase but has no routine (A-23).
+__device__ int narrow_pair(const Model& M, int pi, const R* spq, R slop, R* cand) {
+  const int i = M.p_i[pi], j = M.p_j[pi], code = M.p_code[pi];
+  const int ki = M.s_kind[i], kj = M.s_kind[j];
+  const int mc = pair_maxc(code);
+  for (int k = 0; k < mc; ++k) cand[8 * k + 7] = -1.0;
+  V3<R> pI = ld3(spq + 7 * i), pJ = ld3(spq + 7 * j);
+  bool near;
+  if (ki == BS_KIND_PLANE || kj == BS_KIND_PLANE) {
+    int pl = kj == BS_KIND_PLANE ? j : i, ot = kj == BS_KIND_PLANE ? i : j;
+    V3<R> n = quat_rotate(ld4(spq + 7 * pl + 3), v3(0, 0, 1));
+    near = dot(n, sub(ld3(spq + 7 * ot), ld3(spq + 7 * pl))) <= M.s_radius[ot] + slop;
+  } else {
+    V3<R> d = sub(pI, pJ);
+    near = sqrt(dot(d, d)) <= (M.s_radius[i] + M.s_radius[j]) + slop;
+  }
+  if (!near) return 0;
+  const int base = code & 15;
+  if (base == BS_PAIR_UNSUPPORTED) return 1;
+  const bool flip = (code & BS_PAIR_SWAP) != 0;
+  const int a = flip ? j : i, b = flip ? i : j;
+  const R* sa = M.s_size + 3 * a;
+  const R* sb = M.s_size + 3 * b;
+  const V3<R> pa = ld3(spq + 7 * a), pb = ld3(spq + 7 * b);
+  const Q4<R> qa = ld4(spq + 7 * a + 3), qb = ld4(spq + 7 * b + 3);
+  if (base == BS_PAIR_SPHERE_PLANE) {
+    V3<R> n = quat_rotate(qb, v3(0, 0, 1));
+    R sd = dot(n, sub(pa, pb));
+    put_cand(cand, sub(pa, scl(n, sd)), n, sa[0] - sd, pi, flip, slop);
+  } else if (base == BS_PAIR_BOX_PLANE) {
+    V3<R> n = quat_rotate(qb, v3(0, 0, 1));
+    R dep[8];
+    V3<R> sB[8];
+    int valid = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      V3<R> loc = v3((k & 1) ? sa[0] : -sa[0], (k & 2) ? sa[1] : -sa[1], (k & 4) ? sa[2] : -sa[2]);
+      V3<R> corner = add(pa, quat_rotate(qa, loc));
+      R sd = dot(n, sub(corner, pb));
+      dep[k] = -sd;
+      sB[k] = sub(corner, scl(n, sd));
+      valid += dep[k] >= -slop;
+    }
+    if (valid > 4) {  // keep the four deepest, ties -> lower corner index (A-4)
+      R keep[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        int rank = 0;
+#pragma unroll
+        for (int o = 0; o < 8; ++o) rank += (dep[o] > dep[k]) || (dep[o] == dep[k] && o < k);
+        keep[k] = (dep[k] >= -slop && rank >= 4) ? -INFINITY : dep[k];
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) dep[k] = keep[k];
+    }
+    int w = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (dep[k] >= -slop && w < 4) put_cand(cand + 8 * (w++), sB[k], n, dep[k], pi, flip, slop);
+    }
+  } else if (base == BS_PAIR_SPHERE_SPHERE) {
+    V3<R> d = sub(pa, pb);
+    R dist = sqrt(dot(d, d));
+    V3<R> n = v3(0, 0, 1);
+    if (dist > 1e-12) {
+      R inv = 1.0 / dist;
+      n = v3(d.x * inv, d.y * inv, d.z * inv);
+    }
+    R depth = (sa[0] + sb[0]) - dist;
+    put_cand(cand, add(pb, scl(n, sb[0])), n, depth, pi, flip, slop);
+  } else if (base == BS_PAIR_SPHERE_BOX) {
+    V3<R> loc = quat_rotate(qconj(qb), sub(pa, pb));
+    R h[3] = {sb[0], sb[1], sb[2]};
+    R l3[3] = {loc.x, loc.y, loc.z};
+    R cl[3], dl[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      cl[k] = fmin(fmax(l3[k], -h[k]), h[k]);
+      dl[k] = l3[k] - cl[k];
+    }
+    R d2 = (dl[0] * dl[0] + dl[1] * dl[1]) + dl[2] * dl[2];
+    R nl[3], sl[3], depth;
+    if (d2 > 1e-24) {
+      R dist = sqrt(d2);
+      R inv = 1.0 / dist;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) { nl[k] = dl[k] * inv; sl[k] = cl[k]; }
+      depth = sa[0] - dist;
+    } else {
+      int kk = 0;
+      R best = h[0] - fabs(l3[0]);
+#pragma unroll
+      for (int k = 1; k < 3; ++k) {
+        R pen = h[k] - fabs(l3[k]);
+        if (pen < best) { best = pen; kk = k; }
+      }
+      R sg = l3[kk] >= 0.0 ? 1.0 : -1.0;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) { nl[k] = k == kk ? sg : 0.0; sl[k] = k == kk ? sg * h[kk] : l3[k]; }
+      depth = sa[0] + best;
+    }
+    V3<R> n = quat_rotate(qb, v3(nl[0], nl[1], nl[2]));
+    V3<R> s = add(pb, quat_rotate(qb, v3(sl[0], sl[1], sl[2])));
+    put_cand(cand, s, n, depth, pi, flip, slop);
+  } else if (base == BS_PAIR_CAPSULE_PLANE) {
+    V3<R> n = quat_rotate(qb, v3(0, 0, 1));
+    int w = 0;
+    for (int k = 0; k < 2; ++k) {
+      V3<R> e = add(pa, quat_rotate(qa, v3(0, 0, k ? sa[1] : -sa[1])));
+      R sd = dot(n, sub(e, pb));
+      R depth = sa[0] - sd;
+      if (depth >= -slop) put_cand(cand + 8 * (w++), sub(e, scl(n, sd)), n, depth, pi, flip, slop);
+    }
+  }
+  return 0;
+}
+
+// ------------------------------------------------------------------ group-cooperative FK
+// Lanes build each link's local transform (joint origin o joint motion, with the sincos),
+// then lane 0 walks the topological order composing parent o local.
+template <int G>
+__device__ __forceinline__ void fk_group(const Model& M, const Lay& Y, R* E, int l) {
+  R* Tl = E + Y.Tl;
+  R* lpq = E + Y.lpq;
+  for (int k = l; k < M.L; k += G) {
+    const R* o = M.org + 7 * k;
+    V3<R> tp = ld3(o);
+    Q4<R> tq = ld4(o + 3);
+    const int jt = M.jtype[k];
+    if (jt != BS_JOINT_FIXED) {
+      const R qv = E[Y.q + M.dof[k]];
+      const V3<R> ax = ld3(M.axis + 3 * k);
+      if (jt == BS_JOINT_REVOLUTE) {
+        R s, c;
+        sincos(0.5 * qv, &s, &c);
+        compose_f(tp, tq, v3(0, 0, 0), Q4<R>{c, ax.x * s, ax.y * s, ax.z * s}, tp, tq);
+      } else {
+        tp = add(tp, quat_rotate(tq, scl(ax, qv)));
+      }
+    }
+    st7(Tl + 7 * k, tp, tq);
+  }
+  __syncwarp();
+  if (l == 0) {
+    for (int k = 0; k < M.L; ++k) {
+      const int par = M.parent[k];
+      V3<R> p = ld3(Tl + 7 * k);
+      Q4<R> q = ld4(Tl + 7 * k + 3);
+      if (par >= 0) compose_f(ld3(lpq + 7 * par), ld4(lpq + 7 * par + 3), p, q, p, q);
+      st7(lpq + 7 * k, p, q);
+    }
+  }
+  __syncwarp();
+}
+
+// ------------------------------------------------------------------ one substep
+template <class K>
+__device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E, const int l, const int g,
+                        bool& diverged, int& unsupported, int& nc) {
+  constexpr int G = K::G, MD = K::MD, MA = K::MA;
+  const R dt = P.dt;
+  const int L = M.L, D = M.D, A = M.A, NS = M.S, Dm = Y.Dm;
+  R* lpq = E + Y.lpq;
+  R* Sv = E + Y.Sv;
+  R* In = E + Y.In;
+  R* spq = E + Y.spq;
+  R* Mt = E + Y.Mt;
+  R* Minv = E + Y.Minv;
+  R* cb = E + Y.cb;
+  R* V = E + Y.V;
+  R* Ac = E + Y.Ac;
+  R* F = E + Y.F;
+
+  fk_group<G>(M, Y, E, l);
+
+  // ---- A: per-link motion subspace + world inertia, per-shape world pose, per-actor free
+  //         motion (gyroscopic + gravity), zero the mass matrix
+  const V3<R> grav = v3(P.gravity[0], P.gravity[1], P.gravity[2]);
+  for (int i = l; i < D * Dm; i += G) Mt[i] = 0.0;
+  for (int t = l; t < L + NS + A; t += G) {
+    if (t < L) {
+      const int k = t, jt = M.jtype[k];
+      const V3<R> p = ld3(lpq + 7 * k);
+      const Q4<R> q = ld4(lpq + 7 * k + 3);
+      V3<R> w = v3(0, 0, 0), v = v3(0, 0, 0);
+      if (jt != BS_JOINT_FIXED) {
+        V3<R> a = quat_rotate(q, ld3(M.axis + 3 * k));
+        if (jt == BS_JOINT_REVOLUTE) { w = a; v = crs(p, a); } else { v = a; }
+      }
+      st3(Sv + 6 * k, w);
+      st3(Sv + 6 * k + 3, v);
+      stI(In + 10 * k, world_inertia(M, k, p, q));
+    } else if (t < L + NS) {
+      const int s = t - L;
+      const R* f = M.s_frame + 7 * s;
+      const int bt = M.s_btype[s], bi = M.s_body[s];
+      V3<R> sp;
+      Q4<R> sq;
+      if (bt == BS_BODY_LINK) compose_f(ld3(lpq + 7 * bi), ld4(lpq + 7 * bi + 3), ld3(f), ld4(f + 3), sp, sq);
+      else if (bt == BS_BODY_ACTOR) { sp = ld3(E + Y.apose + 7 * bi); sq = ld4(E + Y.apose + 7 * bi + 3); }
+      else { sp = ld3(f); sq = ld4(f + 3); }
+      st7(spq + 7 * s, sp, sq);
+    } else {
+      const int a = t - L - NS;
+      const Q4<R> aq = ld4(E + Y.apose + 7 * a + 3);
+      const V3<R> av = ld3(E + Y.avel + 6 * a), aw = ld3(E + Y.avel + 6 * a + 3);
+      R Iw[9], Iwi[9];
+      actor_inertia_f(M.a_inertia + 3 * a, aq, Iw, Iwi);
+      V3<R> gyro = scl(crs(aw, m3mul(Iw, aw)), -1.0);
+      st3(E + Y.uw + 3 * a, add(aw, scl(m3mul(Iwi, gyro), dt)));
+      st3(E + Y.uv + 3 * a, add(av, scl(grav, dt)));
+#pragma unroll
+      for (int j = 0; j < 9; ++j) E[Y.Iwi + 9 * a + j] = Iwi[j];
+    }
+  }
+  __syncwarp();
+
+  // ---- B: RNEA forward pass (serial over the topological order)
+  if (l == 0) {
+    const V6 g6 = {{0, 0, 0}, {-P.gravity[0], -P.gravity[1], -P.gravity[2]}};
+    for (int k = 0; k < L; ++k) {
+      const int par = M.parent[k];
+      V6 Vk = par >= 0 ? ld6(V + 6 * par) : V6{{0, 0, 0}, {0, 0, 0}};
+      V6 ak = par >= 0 ? ld6(Ac + 6 * par) : g6;
+      if (M.jtype[k] != BS_JOINT_FIXED) {
+        const R s = E[Y.qd + M.dof[k]];
+        const V6 Sk = ld6(Sv + 6 * k);
+        const V6 Sq = mk6(scl(gw(Sk), s), scl(gv(Sk), s));
+        Vk = add6(Vk, Sq);
+        ak = add6(ak, crossm(Vk, Sq));
+      }
+      st6(V + 6 * k, Vk);
+      st6(Ac + 6 * k, ak);
+    }
+  }
+  __syncwarp();
+  // ---- C: link forces F = I a + V x* I V (parallel over links)
+  for (int k = l; k < L; k += G) {
+    const Inertia I = ldI(In + 10 * k);
+    const V6 Vk = ld6(V + 6 * k);
+    st6(F + 6 * k, add6(imul(I, ld6(Ac + 6 * k)), crossf(Vk, imul(I, Vk))));
+  }
+  __syncwarp();
+  // ---- D: backward pass: bias forces C(q, qd) and composite inertias
+  if (l == 0) {
+    for (int k = L - 1; k >= 0; --k) {
+      const V6 Fk = ld6(F + 6 * k);
+      if (M.jtype[k] != BS_JOINT_FIXED) cb[M.dof[k]] = dot6(ld6(Sv + 6 * k), Fk);
+      const int par = M.parent[k];
+      if (par >= 0) {
+        st6(F + 6 * par, add6(ld6(F + 6 * par), Fk));
+        R* ip = In + 10 * par;
+        const R* ik = In + 10 * k;
+#pragma unroll
+        for (int j = 0; j < 10; ++j) ip[j] += ik[j];
+      }
+    }
+  }
+  __syncwarp();
+  // ---- E: CRBA mass matrix (parallel over dof links)
+  for (int k = l; k < L; k += G) {
+    if (M.jtype[k] == BS_JOINT_FIXED) continue;
+    const int i = M.dof[k];
+    const V6 Fc = imul(ldI(In + 10 * k), ld6(Sv + 6 * k));
+    for (int j = k; j >= 0; j = M.parent[j]) {
+      if (M.jtype[j] == BS_JOINT_FIXED) continue;
+      const int dj = M.dof[j];
+      const R v = dot6(ld6(Sv + 6 * j), Fc);
+      Mt[i * Dm + dj] = v;
+      Mt[dj * Dm + i] = v;
+    }
+  }
+  __syncwarp();
+  // ---- F: implicit PD drives (A-16) and Cholesky of Mt (lane 0; inverse diagonal kept)
+  if (l == 0) {
+    for (int i = 0; i < D; ++i) {
+      const R kp = M.kp[i], kd = M.kd[i], dmp = M.damping[i], fl = M.flim[i];
+      const R qi = E[Y.q + i], qdi = E[Y.qd + i];
+      Mt[i * Dm + i] += dt * (kd + dmp) + (dt * dt) * kp;
+      R tau = kp * ((E[Y.tgt + i] - qi) - dt * qdi) + kd * (0.0 - qdi);
+      tau = fmin(fmax(tau, -fl), fl) - dmp * qdi;
+      cb[i] = tau - cb[i];
+    }
+    for (int j = 0; j < D; ++j) {
+      R s = Mt[j * Dm + j];
+      for (int k = 0; k < j; ++k) s -= Mt[j * Dm + k] * Mt[j * Dm + k];
+      const R inv = rsqrt(s);
+      Mt[j * Dm + j] = inv;  // keep 1 / L_jj
+      for (int i = j + 1; i < D; ++i) {
+        R t = Mt[i * Dm + j];
+        for (int k = 0; k < j; ++k) t -= Mt[i * Dm + k] * Mt[j * Dm + k];
+        Mt[i * Dm + j] = t * inv;
+      }
+    }
+  }
+  __syncwarp();
+  // ---- G: columns of M^-1 (lanes j < D) and the unconstrained velocity (lane D)
+  for (int j = l; j <= D; j += G) {
+    R x[MD];
+#pragma unroll
+    for (int i = 0; i < MD; ++i) x[i] = j < D ? (i == j ? 1.0 : 0.0) : (i < D ? cb[i] : 0.0);
+#pragma unroll
+    for (int i = 0; i < MD; ++i) {
+      if (i < D) {
+        R t = x[i];
+#pragma unroll
+        for (int k = 0; k < i; ++k) t -= Mt[i * Dm + k] * x[k];
+        x[i] = t * Mt[i * Dm + i];
+      }
+    }
+#pragma unroll
+    for (int i = MD - 1; i >= 0; --i) {
+      if (i < D) {
+        R t = x[i];
+#pragma unroll
+        for (int k = i + 1; k < MD; ++k)
+          if (k < D) t -= Mt[k * Dm + i] * x[k];
+        x[i] = t * Mt[i * Dm + i];
+      }
+    }
+    if (j < D) {
+#pragma unroll
+      for (int i = 0; i < MD; ++i)
+        if (i < D) Minv[i * Dm + j] = x[i];
+    } else {
+#pragma unroll
+      for (int i = 0; i < MD; ++i)
+        if (i < D) E[Y.uq + i] = E[Y.qd + i] + dt * x[i];
+    }
+  }
+  // ---- H: broadphase + narrowphase into fixed per-pair candidate slots (A-5)
+  R* cand = E + Y.rows;  // candidates alias the (not yet built) row storage
+  const R slop = P.slop;
+  for (int s = l; s < Y.Cm; s += G) cand[8 * s + 7] = -1.0;
+  __syncwarp();
+  int unsup = 0;
+  for (int pi = l; pi < M.P; pi += G) {
+    int base = 0;
+    for (int q2 = 0; q2 < pi; ++q2) base += pair_maxc(M.p_code[q2]);
+    unsup += narrow_pair(M, pi, spq, slop, cand + 8 * base);
+  }
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) unsup += __shfl_xor_sync(FULLMASK, unsup, o);
+  unsupported = unsup;
+  __syncwarp();
+  // ---- I: ordered compaction of the valid slots (ballot + popc within the group)
+  R* ct = E + Y.ct;
+  {
+    int base = 0;
+    const unsigned gmask = G == 32 ? FULLMASK : ((1u << G) - 1u);
+    for (int k = 0; k < Y.KCH; ++k) {
+      const int s = k * G + l;
+      const bool v = s < Y.Cm && cand[8 * s + 7] >= 0.0;
+      const unsigned bal = (__ballot_sync(FULLMASK, v) >> (g * G)) & gmask;
+      if (v) {
+        const int pos = base + __popc(bal & ((1u << l) - 1u));
+#pragma unroll
+        for (int j = 0; j < 8; ++j) ct[8 * pos + j] = cand[8 * s + j];
+      }
+      base += __popc(bal);
+    }
+    nc = base;
+  }
+  __syncwarp();
+  // ---- J: constraint rows (normal, t1, t2 per contact; parallel over rows)
+  R* rows = E + Y.rows;
+  const int RW = Y.RW, NU = Y.NU;
+  for (int r = l; r < 3 * nc; r += G) {
+    const int c = r / 3, rr = r - 3 * c;
+    const R* cc = ct + 8 * c;
+    const V3<R> Pc = ld3(cc), n = ld3(cc + 3);
+    const R depth = cc[6];
+    const int pi = (int)cc[7];
+    V3<R> dir = n;
+    if (rr) {  // tangent basis (A-6)
+      const R an[3] = {fabs(n.x), fabs(n.y), fabs(n.z)};
+      int k = 0;
+      if (an[1] < an[k]) k = 1;
+      if (an[2] < an[k]) k = 2;
+      V3<R> t1 = crs(n, v3(k == 0, k == 1, k == 2));
+      t1 = scl(t1, rsqrt(dot(t1, t1)));
+      dir = rr == 1 ? t1 : crs(n, t1);
+    }
+    R* row = rows + r * RW;
+    R* J = row + ROW_J;
+    R* W = J + NU;
+    for (int k = 0; k < NU; ++k) { J[k] = 0.0; W[k] = 0.0; }
+    const int slots[2] = {M.p_i[pi], M.p_j[pi]};
+    R Kc = 0.0;
+    for (int s = 0; s < 2; ++s) {
+      const R sg = s ? -1.0 : 1.0;
+      const int sl = slots[s], bt = M.s_btype[sl], bi = M.s_body[sl];
+      if (bt == BS_BODY_LINK && !M.grounded[bi]) {
+        for (int kk = bi; kk >= 0; kk = M.parent[kk]) {
+          if (M.jtype[kk] == BS_JOINT_FIXED) continue;
+          const V3<R> col = add(ld3(Sv + 6 * kk + 3), crs(ld3(Sv + 6 * kk), Pc));
+          J[M.dof[kk]] += sg * dot(dir, col);
+        }
+      } else if (bt == BS_BODY_ACTOR) {
+        R* Jb = J + Dm + 6 * bi;
+        R* Wb = W + Dm + 6 * bi;
+        const R invm = 1.0 / M.a_mass[bi];
+        const V3<R> Jv = scl(dir, sg);
+        const V3<R> Jw = scl(crs(sub(Pc, ld3(E + Y.apose + 7 * bi)), dir), sg);
+        const V3<R> Wv = scl(Jv, invm);
+        const V3<R> Ww = m3mul(E + Y.Iwi + 9 * bi, Jw);
+        st3(Jb, Jv); st3(Jb + 3, Jw);
+        st3(Wb, Wv); st3(Wb + 3, Ww);
+        Kc += dot(dir, dir) * invm + dot(Jw, Ww);
+      }
+    }
+    R KA = 0.0;
+    for (int i = 0; i < D; ++i) {
+      R w = 0.0;
+      for (int k = 0; k < D; ++k) w += Minv[i * Dm + k] * J[k];
+      W[i] = w;
+      KA += J[i] * w;
+    }
+    Kc = KA + Kc;
+    row[0] = Kc > 1e-12 ? 1.0 / Kc : 0.0;
+    row[1] = 0.0;
+    row[2] = depth > slop ? P.beta * (depth - slop) / dt : (depth >= 0.0 ? 0.0 : depth / dt);
+    row[3] = depth < 0.0 ? depth / dt : 0.0;
+  }
+  __syncwarp();
+
+  // ---- K: projected Gauss-Seidel, sequential row order, executed by every
+  //         lane of the group on a register copy of u (identical in every lane afterwards)
+  constexpr int NUM = K::NU;
+  R u[NUM];
+#pragma unroll
+  for (int k = 0; k < NUM; ++k) {
+    R x = 0.0;
+    if (k < Dm) x = k < D ? E[Y.uq + k] : 0.0;
+    else if (k < NU) {
+      const int a = (k - Dm) / 6, j = (k - Dm) - 6 * a;
+      if (a < A) x = j < 3 ? E[Y.uv + 3 * a + j] : E[Y.uw + 3 * a + j - 3];
+    }
+    u[k] = x;
+  }
+  const int iters = P.pos_iters + P.vel_iters;
+  const R mu = P.friction;
+  for (int it = 0; it < iters; ++it) {
+    const bool pos_phase = it < P.pos_iters;
+    const R* row = rows;
+    for (int c = 0; c < nc; ++c) {
+      R lam_n = 0.0;
+#pragma unroll
+      for (int rr = 0; rr < 3; ++rr, row += RW) {
+        const R invK = row[0];
+        const R old = row[1];
+        if (invK == 0.0) {
+          if (rr == 0) lam_n = old;
+          continue;
+        }
+        const R* J = row + ROW_J;
+        const R* Wr = J + NU;
+        R v0 = 0.0, v1 = 0.0;  // two partial sums for ILP
+#pragma unroll
+        for (int k = 0; k < NUM; k += 2) {
+          if (k < NU) v0 += J[k] * u[k];
+          if (k + 1 < NUM && k + 1 < NU) v1 += J[k + 1] * u[k + 1];
+        }
+        const R v = v0 + v1;
+        R nw;
+        if (rr == 0) {
+          const R tgt = pos_phase ? row[2] : row[3];
+          nw = fmax(old + (tgt - v) * invK, 0.0);
+          lam_n = nw;
+        } else {
+          const R bound = mu * lam_n;
+          nw = fmin(fmax(old + (0.0 - v) * invK, -bound), bound);
+        }
+        const R delta = nw - old;
+        const_cast<R*>(row)[1] = nw;  // every lane stores the same value and reads back its own
+#pragma unroll
+        for (int k = 0; k < NUM; ++k)
+          if (k < NU) u[k] += delta * Wr[k];
+      }
+    }
+  }
+
+  // ---- L: semi-implicit Euler, joint limits (A-7), actor orientation (A-8), divergence
+  //         freeze.  Every lane holds the same velocities, so every lane
+  //         evaluates the update; lanes then write disjoint entries.
+  R q1[MD], qd1[MD];
+  bool finite = true;
+#pragma unroll
+  for (int i = 0; i < MD; ++i) {
+    if (i < D) {
+      R v = E[Y.q + i] + dt * u[i];
+      R w = u[i];
+      const R lo = M.lower[i], hi = M.upper[i];
+      if (v < lo) { v = lo; w = fmax(w, 0.0); }
+      else if (v > hi) { v = hi; w = fmin(w, 0.0); }
+      q1[i] = v;
+      qd1[i] = w;
+      finite &= isfinite(v) && isfinite(w);
+    }
+  }
+  V3<R> ap1[MA], uva[MA], uwa[MA];
+  Q4<R> aq1[MA];
+#pragma unroll
+  for (int a = 0; a < MA; ++a) {
+    if (a < A) {
+      // u index of actor a's block: Dm + 6a (Dm may be < MD, so select at run time)
+      R blk[6];
+#pragma unroll
+      for (int j = 0; j < 6; ++j) {
+        R x = 0.0;
+#pragma unroll
+        for (int k = 0; k < NUM; ++k)
+          if (k == Dm + 6 * a + j) x = u[k];
+        blk[j] = x;
+      }
+      uva[a] = v3(blk[0], blk[1], blk[2]);
+      uwa[a] = v3(blk[3], blk[4], blk[5]);
+      const V3<R> ap = ld3(E + Y.apose + 7 * a);
+      const Q4<R> aq = ld4(E + Y.apose + 7 * a + 3);
+      ap1[a] = v3(ap.x + uva[a].x * dt, ap.y + uva[a].y * dt, ap.z + uva[a].z * dt);
+      const Q4<R> wq = quat_mul(Q4<R>{0.0, uwa[a].x, uwa[a].y, uwa[a].z}, aq);
+      const R h = 0.5 * dt;
+      aq1[a] = qnorm_f(Q4<R>{aq.w + h * wq.w, aq.x + h * wq.x, aq.y + h * wq.y, aq.z + h * wq.z});
+      finite &= isfinite(ap1[a].x) && isfinite(ap1[a].y) && isfinite(ap1[a].z);
+      finite &= isfinite(aq1[a].w) && isfinite(aq1[a].x) && isfinite(aq1[a].y) && isfinite(aq1[a].z);
+#pragma unroll
+      for (int j = 0; j < 6; ++j) finite &= isfinite(blk[j]);
+    }
+  }
+  __syncwarp();  // every lane has read q / actor poses before any lane overwrites them
+  if (!finite) diverged = true;
+  if (!diverged) {
+#pragma unroll
+    for (int i = 0; i < MD; ++i)
+      if (i < D && (i % G) == l) { E[Y.q + i] = q1[i]; E[Y.qd + i] = qd1[i]; }
+#pragma unroll
+    for (int a = 0; a < MA; ++a)
+      if (a < A && (a % G) == l) {
+        st7(E + Y.apose + 7 * a, ap1[a], aq1[a]);
+        st3(E + Y.avel + 6 * a, uva[a]);
+        st3(E + Y.avel + 6 * a + 3, uwa[a]);
+      }
+  }
+  __syncwarp();
+}
+
+// ------------------------------------------------------------------ the kernel
+template <class K>
+__global__ void __launch_bounds__(32) k_step(BsModelTables T, BsEnvState S, BsStepOutputs O, BsSimParams P,
+                                             const float* __restrict__ action, Lay Y) {
+  constexpr int G = K::G, MD = K::MD, MA = K::MA, EPW = K::EPW;
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x;
+  const int g = lane / G, l = lane - g * G;
+  const int e_raw = blockIdx.x * EPW + g;
+  const bool live = e_raw < S.num_envs;
+  const int e = live ? e_raw : S.num_envs - 1;  // idle groups shadow the last env, never store
+  R* E = smem + g * Y.total;
+  const Model M = model_of(T, S.model_id[e]);
+  const int Dm = Y.Dm, Am = Y.Am;
+
+  // ---- stage the env's state rows
+  for (int i = l; i < Dm; i += G) {
+    E[Y.q + i] = S.qpos[(int64_t)e * Dm + i];
+    E[Y.qd + i] = S.qvel[(int64_t)e * Dm + i];
+  }
+  for (int i = l; i < 7 * Am; i += G) E[Y.apose + i] = S.actor_pose[(int64_t)e * 7 * Am + i];
+  for (int i = l; i < 6 * Am; i += G) E[Y.avel + i] = S.actor_vel[(int64_t)e * 6 * Am + i];
+  if (l < 3) E[Y.goal + l] = S.goal[3 * (int64_t)e + l];
+  // ---- controller: drive targets, once per control step
+  const float* act = action + (int64_t)e * P.action_dim;
+  for (int i = l; i < M.D; i += G) {
+    const int ai = M.ctrl[i];
+    const R qi = S.qpos[(int64_t)e * Dm + i];
+    R tgt = qi;
+    if (ai >= 0) {
+      const R a = fmin(fmax((R)act[ai], -1.0), 1.0);
+      const R lo = M.lower[i], hi = M.upper[i];
+      if (P.ctrl_mode == BS_CTRL_PD_JOINT_DELTA_POS) {
+        tgt = fmin(fmax(qi + a * P.action_scale, lo), hi);
+      } else {
+        const R un = (isfinite(lo) && isfinite(hi)) ? lo + (a + 1.0) * 0.5 * (hi - lo) : a * P.action_scale;
+        tgt = fmin(fmax(un, lo), hi);
+      }
+    }
+    E[Y.tgt + i] = tgt;
+  }
+  bool diverged = S.diverged[e] != 0;
+  __syncwarp();
+
+  int unsupported = 0, nc = 0;
+  for (int s = 0; s < P.substeps; ++s) {
+    substep<K>(M, P, Y, E, l, g, diverged, unsupported, nc);
+    if (s == P.substeps - 1 && O.contact_count && live) {  // ContactSet of the last substep
+      const R* ct = E + Y.ct;
+      for (int c = l; c < nc && c < T.C_max; c += G) {
+        const int64_t o = (int64_t)e * T.C_max + c;
+        const int pi = (int)ct[8 * c + 7];
+        if (O.contact_pairs) { O.contact_pairs[2 * o] = M.p_i[pi]; O.contact_pairs[2 * o + 1] = M.p_j[pi]; }
+        if (O.contact_geom) {
+#pragma unroll
+          for (int j = 0; j < 7; ++j) O.contact_geom[7 * o + j] = ct[8 * c + j];
+        }
+      }
+      if (l == 0) O.contact_count[e] = nc;
+    }
+  }
+  fk_group<G>(M, Y, E, l);
+
+  // ---- task evaluation; every lane evaluates (cheap, uniform)
+  const R* lpq = E + Y.lpq;
+  float reward = 0.0f;
+  bool success = false, fail = diverged;
+  int32_t tdof = S.target_dof[e];
+  if (P.task == BS_TASK_PICKCUBE) {
+    const R* f = P.task_f;
+    const V3<R> ee = ld3(lpq + 7 * P.ee_link);
+    const V3<R> cube = ld3(E + Y.apose);
+    const R d_ee = dist3(ee, cube);
+    const R d_goal = dist3(v3(cube.x, cube.y, 0.0), v3(E[Y.goal], E[Y.goal + 1], 0.0));
+    success = d_goal < f[4];
+    fail = cube.z < f[5] || diverged;
+    reward = (float)(-__dadd_rn(d_ee, d_goal));
+  } else if (P.task == BS_TASK_OPENCHAIN) {
+    const R hi = tdof >= 0 ? M.upper[tdof] : 1.0;
+    const R qv = tdof >= 0 ? E[Y.q + tdof] : 0.0;
+    success = tdof >= 0 && qv > P.task_f[1] * hi;
+    reward = (float)(tdof >= 0 ? qv / hi : 0.0);
+  }
+  int32_t el = S.elapsed[e] + 1;
+  const bool terminated = P.early_termination ? (success || fail) : false;
+  const bool truncated = el >= P.max_steps;
+  if (live && l == 0) {
+    O.reward[e] = reward;
+    O.terminated[e] = terminated;
+    O.truncated[e] = truncated;
+    O.success[e] = success;
+    O.fail[e] = fail;
+    O.unsupported_pairs[e] = unsupported;
+  }
+  // ---- in-kernel auto-reset from the env's Philox stream
+  const bool done = live && P.auto_reset && (terminated || truncated);
+  uint8_t div_out = diverged;
+  if (__any_sync(FULLMASK, done)) {
+    if (done && l == 0) {
+      const uint32_t rc = (uint32_t)S.reset_count[e] + 1u;
+      S.reset_count[e] = rc;
+      R q[MD], qd[MD], goal[3];
+      V3<R> ap[MA], av[MA], aw[MA];
+      Q4<R> aq[MA];
+      task_reset(M, P, S.env_offset + e, rc, q, qd, ap, aq, av, aw, goal, &tdof);
+      S.target_dof[e] = tdof;
+      for (int i = 0; i < M.D; ++i) { E[Y.q + i] = q[i]; E[Y.qd + i] = qd[i]; }
+      for (int a = 0; a < M.A; ++a) {
+        st7(E + Y.apose + 7 * a, ap[a], aq[a]);
+        st3(E + Y.avel + 6 * a, av[a]);
+        st3(E + Y.avel + 6 * a + 3, aw[a]);
+      }
+      for (int k = 0; k < 3; ++k) E[Y.goal + k] = goal[k];
+    }
+    if (done) { el = 0; div_out = 0; }
+    __syncwarp();
+    fk_group<G>(M, Y, E, l);
+  }
+  if (!live) return;
+  // ---- write back the state rows, the FK cache and the state observation
+  for (int i = l; i < Dm; i += G) {
+    S.qpos[(int64_t)e * Dm + i] = E[Y.q + i];
+    S.qvel[(int64_t)e * Dm + i] = E[Y.qd + i];
+    if (i < M.D) S.target[(int64_t)e * Dm + i] = E[Y.tgt + i];
+  }
+  for (int i = l; i < 7 * M.A; i += G) S.actor_pose[(int64_t)e * 7 * Am + i] = E[Y.apose + i];
+  for (int i = l; i < 6 * M.A; i += G) S.actor_vel[(int64_t)e * 6 * Am + i] = E[Y.avel + i];
+  if (l < 3) S.goal[3 * (int64_t)e + l] = E[Y.goal + l];
+  for (int i = l; i < 7 * M.L; i += G) S.link_pose[(int64_t)e * 7 * Y.Lm + i] = lpq[i];
+  if (l == 0) {
+    S.elapsed[e] = el;
+    S.diverged[e] = div_out;
+  }
+  if (O.obs) {
+    // layout: q[D_max] qd[D_max] ee_p[3]
+    //   per actor slot: p[3] q[4] v[3] w[3]   goal[3]   zero padding
+    float* o = O.obs + (int64_t)e * O.obs_dim;
+    const int b_ee = 2 * Dm, b_act = b_ee + 3, b_goal = b_act + 13 * Am;
+    for (int k = l; k < O.obs_dim; k += G) {
+      R v = 0.0;
+      if (k < Dm) v = k < M.D ? E[Y.q + k] : 0.0;
+      else if (k < b_ee) v = (k - Dm) < M.D ? E[Y.qd + k - Dm] : 0.0;
+      else if (k < b_act) v = P.ee_link >= 0 ? lpq[7 * P.ee_link + (k - b_ee)] : 0.0;
+      else if (k < b_goal) {
+        const int a = (k - b_act) / 13, j = (k - b_act) - 13 * a;
+        if (a < M.A) v = j < 7 ? E[Y.apose + 7 * a + j] : E[Y.avel + 6 * a + (j - 7)];
+      } else if (k < b_goal + 3) v = E[Y.goal + (k - b_goal)];
+      o[k] = (float)v;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ host side
+static Lay make_lay(const BsModelTables& T, int G) {
+  Lay y;
+  y.Dm = T.D_max; y.Lm = T.L_max; y.Sm = T.S_max; y.Cm = T.C_max; y.Am = T.A_max;
+  y.NU = y.Dm + 6 * y.Am;
+  y.RW = ROW_J + 2 * y.NU;
+  y.KCH = (y.Cm + G - 1) / G;
+  int o = 0;
+  y.q = o; o += y.Dm;
+  y.qd = o; o += y.Dm;
+  y.tgt = o; o += y.Dm;
+  y.apose = o; o += 7 * y.Am;
+  y.avel = o; o += 6 * y.Am;
+  y.goal = o; o += 3;
+  y.lpq = o; o += 7 * y.Lm;
+  y.Sv = o; o += 6 * y.Lm;
+  y.In = o; o += 10 * y.Lm;
+  y.Mt = o; o += y.Dm * y.Dm;
+  y.Minv = o; o += y.Dm * y.Dm;
+  y.cb = o; o += y.Dm;
+  y.uq = o; o += y.Dm;
+  y.uv = o; o += 3 * y.Am;
+  y.uw = o; o += 3 * y.Am;
+  y.Iwi = o; o += 9 * y.Am;
+  y.spq = o; o += 7 * y.Sm;
+  // union: {FK local transforms + RNEA temporaries} | {compacted contacts}
+  const int fkr = 7 * y.Lm + 18 * y.Lm, cts = 8 * y.Cm;
+  y.Tl = o; y.V = o + 7 * y.Lm; y.Ac = y.V + 6 * y.Lm; y.F = y.Ac + 6 * y.Lm;
+  y.ct = o;
+  o += fkr > cts ? fkr : cts;
+  y.rows = o;
+  const int rws = 3 * y.Cm * y.RW;
+  o += rws > 8 * y.Cm ? rws : 8 * y.Cm;  // row storage doubles as the candidate slots
+  y.total = o;
+  return y;
+}
+
+template <class K>
+static int launch(const BsModelTables& T, const BsEnvState& S, const BsStepOutputs& O, const BsSimParams& P,
+                  const float* action, cudaStream_t st) {
+  const Lay y = make_lay(T, K::G);
+  const size_t bytes = (size_t)K::EPW * y.total * sizeof(double);
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(k_step<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
+      return BS_ERR_CUDA;
+    attr_set = true;
+  }
+  if (bytes > 227 * 1024) return BS_ERR_UNSUPPORTED;
+  const int blocks = (S.num_envs + K::EPW - 1) / K::EPW;
+  k_step<K><<<blocks, 32, bytes, st>>>(T, S, O, P, action, y);
+  return launch_status();
+}
+
+typedef Cfg<8, 4, 1> CfgSmall;    // PickCube-style: D <= 4, one free actor
+typedef Cfg<8, 12, 4> CfgLarge;   // cabinets / heterogeneous scenes
+
+}  // namespace step
+}  // namespace bs
+
+using namespace bs::step;
+
+extern "C" {
+
+int bs_step(const BsModelTables* T, const BsEnvState* S, const BsStepOutputs* O, const BsSimParams* P,
+            const float* action, void* stream) {
+  if (!T || !S || !O || !P || !action) return BS_ERR_ARGUMENT;
+  if (S->num_envs <= 0) return BS_OK;
+  if (!O->reward || !O->terminated || !O->truncated || !O->success || !O->fail || !O->unsupported_pairs)
+    return BS_ERR_ARGUMENT;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (T->D_max <= CfgSmall::MD && T->A_max <= CfgSmall::MA) return launch<CfgSmall>(*T, *S, *O, *P, action, st);
+  if (T->D_max <= CfgLarge::MD && T->A_max <= CfgLarge::MA) return launch<CfgLarge>(*T, *S, *O, *P, action, st);
+  return BS_ERR_UNSUPPORTED;
+}
+
+}  // extern "C"

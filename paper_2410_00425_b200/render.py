@@ -1,0 +1,254 @@
+"""Batched rendering front end: cameras, mesh tables, frame buffers -> ``bs_render``.
+
+Implements the SPEC's render surface on the device:
+
+- ``CameraConfig``: OpenCV axes, world-fixed or mounted on a link.
+- ``randomize_cameras``: per-env pose/intrinsics jitter from the env's
+  counter RNG stream.
+- ``Renderer.render``: one ``bs_render`` launch per camera group. It fills RGB u8 / depth f32 /
+  seg u16 frames (FrameBatch), optionally the fused world-frame pointcloud
+  (SPEC.md:477-485).
+
+Meshes are tessellated on the host once per distinct env layout (meshes.py). Every buffer is a
+CUDA tensor owned here, and the kernel never allocates, so the render launch is captured in the
+env's CUDA graph together with the step.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from . import cabi
+from . import hostmath as hm
+from . import meshes
+from . import rng as brng
+from .errors import DimensionError, InputError
+
+OBS_MODES = ("state", "rgb", "depth", "rgbd", "rgb+depth", "seg", "pointcloud")
+
+
+@dataclass(frozen=True)
+class CameraConfig:
+    """SPEC.md:450.  pose = camera -> world (OpenCV: x right, y down, z forward) or, when
+    `mount` names a link, the camera's offset in that link's frame."""
+
+    name: str = "cam"
+    width: int = 128
+    height: int = 128
+    fx: float = 110.85
+    fy: float = 110.85
+    cx: float = 64.0
+    cy: float = 64.0
+    pose_p: tuple = (0.0, 0.0, 1.0)
+    pose_q: tuple = (1.0, 0.0, 0.0, 0.0)
+    mount: str = None
+    near: float = 0.01
+    far: float = 10.0
+
+    def __post_init__(self):
+        if not (0.0 < self.near < self.far):
+            raise InputError(f"camera {self.name!r}: need 0 < near < far")
+        if self.width < 1 or self.height < 1:
+            raise InputError(f"camera {self.name!r}: width and height must be >= 1")
+
+
+def look_at(eye, target, up=(0.0, 0.0, 1.0)):
+    """Camera -> world quaternion for an OpenCV camera at `eye` looking at `target`."""
+    return tuple(hm.look_at(eye, target, up)[1])
+
+
+def pinhole(width, height, fov_y_deg):
+    fy = (height / 2.0) / math.tan(math.radians(fov_y_deg) / 2.0)
+    return dict(width=width, height=height, fx=fy, fy=fy, cx=width / 2.0, cy=height / 2.0)
+
+
+def default_cameras(width=128, height=128):
+    """PickCube-style tabletop view (BASELINE configs C3/C4: one 128x128 camera)."""
+    eye, target = (0.35, 0.35, 0.45), (-0.15, 0.0, 0.05)
+    return [CameraConfig("base_camera", pose_p=eye, pose_q=look_at(eye, target), **pinhole(width, height, 60.0))]
+
+
+@dataclass(frozen=True)
+class CameraJitter:
+    """randomize_cameras ranges: uniform +-pos (m), +-rot (rad, about a
+    uniformly drawn axis-angle vector's components), +-focal (fraction of fx/fy)."""
+
+    pos: float = 0.0
+    rot: float = 0.0
+    focal: float = 0.0
+
+
+def randomize_cameras(cameras, num_envs, seed, jitter: CameraJitter, env_offset=0):
+    """Per-env camera poses/intrinsics (N, C, 7) f64 and (N, C, 4) f32, drawn from each env's
+    Philox stream (counter = (camera, 0, global env, 'CAMR')); zero jitter -> the base config
+    for every env, bitwise."""
+    C = len(cameras)
+    ids = np.arange(env_offset, env_offset + num_envs, dtype=np.uint64)
+    pose = np.zeros((num_envs, C, 7))
+    intr = np.zeros((num_envs, C, 4), np.float32)
+    for c, cam in enumerate(cameras):
+        base_p = np.asarray(cam.pose_p, np.float64)
+        base_q = hm.qnormalize(cam.pose_q)
+        pose[:, c, :3] = base_p
+        pose[:, c, 3:] = base_q
+        intr[:, c] = (cam.fx, cam.fy, cam.cx, cam.cy)
+        if jitter.pos or jitter.rot or jitter.focal:
+            u = brng.uniforms(seed, ids, c, brng.TAG_CAMERA, 8)   # (N, 8) in [0, 1)
+            pose[:, c, :3] = base_p + jitter.pos * (2.0 * u[:, 0:3] - 1.0)
+            rv = jitter.rot * (2.0 * u[:, 3:6] - 1.0)
+            for e in range(num_envs):
+                ang = float(np.linalg.norm(rv[e]))
+                if ang > 0.0:
+                    ax = rv[e] / ang
+                    dq = np.array([math.cos(ang / 2), *(ax * math.sin(ang / 2))])
+                    pose[e, c, 3:] = hm.qnormalize(hm.qmul(base_q, dq))
+            s = 1.0 + jitter.focal * (2.0 * u[:, 6] - 1.0)
+            intr[:, c, 0] = (cam.fx * s).astype(np.float32)
+            intr[:, c, 1] = (cam.fy * s).astype(np.float32)
+    return pose, intr
+
+
+@dataclass
+class RenderParams:
+    light_dir: tuple = (0.35, 0.25, 1.0)   # towards the light, world frame (normalised)
+    ambient: float = 0.35
+    diffuse: float = 0.65
+    background: tuple = (0.0, 0.0, 0.0)
+    tile: int = 64
+
+
+class MeshTables:
+    """Device mesh tables for every model of a scene (BsMeshTables)."""
+
+    def __init__(self, scene):
+        per = [meshes.model_mesh(m.shapes) for m in scene.models]
+        M = len(per)
+        self.V_max = max(1, max(len(p["verts"]) for p in per))
+        self.T_max = max(1, max(len(p["tris"]) for p in per))
+        verts = np.zeros((M, self.V_max, 3), np.float32)
+        vsh = np.zeros((M, self.V_max), np.int32)
+        tris = np.zeros((M, self.T_max, 3), np.int32)
+        tsh = np.zeros((M, self.T_max), np.int32)
+        nv = np.zeros(M, np.int32)
+        nt = np.zeros(M, np.int32)
+        for i, p in enumerate(per):
+            nv[i], nt[i] = len(p["verts"]), len(p["tris"])
+            verts[i, :nv[i]], vsh[i, :nv[i]] = p["verts"], p["vert_shape"]
+            tris[i, :nt[i]], tsh[i, :nt[i]] = p["tris"], p["tri_shape"]
+        self.host = dict(verts=verts, vert_shape=vsh, tris=tris, tri_shape=tsh, n_verts=nv, n_tris=nt)
+        self.per_model = per
+        dev = scene.device
+        self.t = {k: torch.as_tensor(v, device=dev) for k, v in self.host.items()}
+        c = cabi.BsMeshTables()
+        c.num_models, c.V_max, c.T_max = M, self.V_max, self.T_max
+        for k, v in self.t.items():
+            setattr(c, k, v.data_ptr())
+        self.c = c
+
+
+class Renderer:
+    """Renders every env's cameras into device frame buffers.  Cameras are grouped by
+    resolution; each group is one ``bs_render`` launch (grid = tiles x cameras x envs)."""
+
+    def __init__(self, scene, cameras, obs_mode="rgbd", seed=0, jitter: CameraJitter = CameraJitter(),
+                 params: RenderParams = RenderParams(), env_color=None):
+        if obs_mode not in OBS_MODES:
+            raise InputError(f"unknown obs_mode {obs_mode!r}; one of {OBS_MODES}")
+        self.scene = scene
+        self.cameras = list(cameras)
+        if not self.cameras:
+            raise InputError("a rendering obs mode needs at least one camera")
+        self.obs_mode = obs_mode
+        self.params = params
+        self.mesh = MeshTables(scene)
+        dev, N = scene.device, scene.num_envs
+        want_pc = obs_mode == "pointcloud"
+        self.groups = []
+        for (w, h) in sorted({(c.width, c.height) for c in self.cameras}):
+            cams = [c for c in self.cameras if (c.width, c.height) == (w, h)]
+            if len({(c.near, c.far) for c in cams}) != 1:
+                raise InputError("cameras of one resolution must share near/far planes")
+            pose, intr = randomize_cameras(cams, N, seed, jitter, scene.env_offset)
+            mount = []
+            for c in cams:
+                if c.mount is None:
+                    mount.append(-1)
+                else:
+                    names = scene.models[0].link_names
+                    if c.mount not in names or len(scene.models) > 1 and any(
+                            m.link_names.index(c.mount) != names.index(c.mount) for m in scene.models
+                            if c.mount in m.link_names):
+                        raise InputError(f"camera mount link {c.mount!r} must exist at the same slot in every env")
+                    mount.append(names.index(c.mount))
+            C = len(cams)
+            g = {"cams": cams, "w": w, "h": h,
+                 "pose": torch.as_tensor(pose, device=dev).contiguous(),
+                 "intr": torch.as_tensor(intr, device=dev).contiguous(),
+                 "mount": torch.as_tensor(np.asarray(mount, np.int32), device=dev),
+                 "rgb": torch.zeros((N, C, h, w, 3), dtype=torch.uint8, device=dev),
+                 "depth": torch.zeros((N, C, h, w), dtype=torch.float32, device=dev),
+                 "seg": torch.zeros((N, C, h, w), dtype=torch.int16, device=dev),
+                 "pc": torch.zeros((N, C, h * w, 6), dtype=torch.float32, device=dev) if want_pc else None}
+            cb = cabi.BsCameraBatch()
+            cb.num_cams, cb.width, cb.height = C, w, h
+            cb.near_plane, cb.far_plane = cams[0].near, cams[0].far
+            cb.mount_link, cb.pose, cb.intrinsics = g["mount"].data_ptr(), g["pose"].data_ptr(), g["intr"].data_ptr()
+            g["c_cams"] = cb
+            fb = cabi.BsFrameBatch()
+            fb.rgb, fb.depth, fb.seg = g["rgb"].data_ptr(), g["depth"].data_ptr(), g["seg"].data_ptr()
+            fb.pointcloud = g["pc"].data_ptr() if want_pc else None
+            g["c_out"] = fb
+            self.groups.append(g)
+        rp = cabi.BsRenderParams()
+        L = np.asarray(params.light_dir, np.float64)
+        L = L / math.sqrt(float(L @ L))
+        for i in range(3):
+            rp.light_dir[i] = L[i]
+            rp.background[i] = params.background[i]
+        rp.ambient, rp.diffuse, rp.tile = params.ambient, params.diffuse, params.tile
+        self.c_params = rp
+        self.light = L
+        self.env_color = None
+        if env_color is not None:
+            ec = torch.as_tensor(env_color, dtype=torch.float32, device=dev).contiguous()
+            if ec.shape != (N, scene.S_max, 3):
+                raise DimensionError(f"env_color must be (num_envs, S_max, 3) = ({N}, {scene.S_max}, 3)")
+            self.env_color = ec
+
+    def render(self, scene=None):
+        scene = scene or self.scene
+        ecp = self.env_color.data_ptr() if self.env_color is not None else None
+        for g in self.groups:
+            nat.call("bs_render", ctypes.byref(scene.c_tables), ctypes.byref(scene.c_state),
+                     ctypes.byref(self.mesh.c), ctypes.byref(g["c_cams"]), ecp, ctypes.byref(self.c_params),
+                     ctypes.byref(g["c_out"]), nat.stream_handle())
+
+    def frames(self):
+        """{camera name: {"rgb", "depth", "seg"[, "pointcloud"]}} views of the device buffers."""
+        out = {}
+        for g in self.groups:
+            for i, c in enumerate(g["cams"]):
+                d = {"rgb": g["rgb"][:, i], "depth": g["depth"][:, i], "seg": g["seg"][:, i]}
+                if g["pc"] is not None:
+                    d["pointcloud"] = g["pc"][:, i]
+                out[c.name] = d
+        return out
+
+    def observation(self, obs_mode=None):
+        mode = obs_mode or self.obs_mode
+        fr = self.frames()
+        if mode == "pointcloud":
+            pcs = [f["pointcloud"] for f in fr.values()]
+            pc = torch.cat(pcs, dim=1) if len(pcs) > 1 else pcs[0]
+            segs = [f["seg"].reshape(f["seg"].shape[0], -1) for f in fr.values()]
+            seg = torch.cat(segs, 1) if len(segs) > 1 else segs[0]
+            return {"pointcloud": pc, "pointcloud_mask": seg != 0, "seg": seg}
+        keep = {"rgb": ("rgb",), "depth": ("depth",), "rgbd": ("rgb", "depth"), "rgb+depth": ("rgb", "depth"),
+                "seg": ("seg",)}[mode]
+        return {"sensor_data": {name: {k: f[k] for k in keep + ("seg",)} for name, f in fr.items()}}
