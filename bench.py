@@ -1,24 +1,34 @@
-"""Benchmark: env-steps/s of the PickCube-style tabletop task (BASELINE.json configs[1], "C2":
-state obs, 4096 envs per GPU, sim 120 Hz / control 60 Hz, 4 position iterations) on N B200s,
-next to the reference CPU path timed on the host cores.
+"""Benchmark: env-steps/s of the PickCube-style tabletop task on N B200s, next to the reference
+CPU path timed on the host cores.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2|c3|c4]
   (N>1: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...)
 
-One "step" = one env.step over every env on every GPU (controller -> 2 substeps of dynamics,
-contacts, PGS -> FK -> reward/termination -> state obs -> auto-reset), fed by 1000-style
-uniform random actions.  Timing rules:
-  * `value`: device time (CUDA events on the launching stream) summed over K steps, inputs
-    resident in HBM; the L2 is flushed (256 MiB write) BEFORE every timed step, outside
-    the events, so every step starts cold.  Max over ranks; whole-job env-steps/s.
-  * `e2e`: the public API (`Env.step(host action)`) with the action copied from pinned
-    host memory and obs + reward copied back every step; wall clock, synchronised.
-  * `roofline`: the fused step kernel alone (events around its launch), algorithmic bytes
-    per env-step / duration vs MEASURED_PEAKS.json hbm_gbs.
-  * `cpu_baseline` (rank 0, N=1 only): the oracle (CPU restatement of the reference path,
-    numpy) on all host cores, one process per core, for ~10 s.
+Workloads (BASELINE.json configs):
+- c2 (the headline, configs[1]): state obs, 4096 envs per GPU;
+- c3 (configs[2]): obs_mode rgb+depth (+seg), one 128x128 camera, 1024 envs per GPU;
+- c4: pointcloud obs from one 128x128 camera, 1024 envs per GPU.
+The default run prints the c2 line and attaches a shorter c3 measurement under
+"secondary".
+
+One "step" = one env.step over every env on every GPU. That is: controller -> 2 substeps of
+dynamics, contacts and PGS -> FK -> reward/termination -> state obs -> auto-reset, plus the
+render for camera workloads. Steps are fed by uniform random actions.
+
+Timing rules:
+- `value`: device time (CUDA events on the launching stream) summed over K steps, with inputs
+  resident in HBM. The L2 is flushed (a 256 MiB write) BEFORE every timed step, outside the
+  events, so every step starts cold. The max is taken over ranks; the figure is whole-job
+  env-steps/s.
+- `e2e`: the public API (`Env.step(host action)`). The action is copied from pinned host
+  memory, and obs + reward are copied back every step. Wall clock, synchronised.
+- `roofline`: the dominant kernel alone (events around its launch). Algorithmic bytes per
+  env-step / duration, against MEASURED_PEAKS.json hbm_gbs.
+- `cpu_baseline` (rank 0, N=1 only): the oracle (CPU restatement of the reference path,
+  numpy) on all host cores, one process per core, for a bounded sample.
 The reference arm (`--impl reference`) times that same CPU path per step on the same
-workload.  NCCL is used only after the timed region, for rollout statistics.
+workload. NCCL is used only after the timed region: the max-over-ranks timing and the rollout
+statistics.
 """
 
 from __future__ import annotations
@@ -34,10 +44,16 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
-ENVS_PER_GPU = 4096
 METRIC = "env-steps/s (sim+render, whole box)"
-WORKLOAD = "C2 PickCube-style (ARM3 + cube + ground), obs_mode=state, 4096 envs/GPU"
 FALLBACK_HBM_GBS = 6650.0
+WORKLOADS = {
+    "c2": {"envs": 4096, "obs_mode": "state",
+           "desc": "C2 PickCube-style (ARM3 + cube + ground), obs_mode=state, 4096 envs/GPU"},
+    "c3": {"envs": 1024, "obs_mode": "rgbd",
+           "desc": "C3 PickCube-style, obs_mode=rgb+depth (+seg) 1 camera 128x128, 1024 envs/GPU"},
+    "c4": {"envs": 1024, "obs_mode": "pointcloud",
+           "desc": "C4-style PickCube, obs_mode=pointcloud (+seg mask) 1 camera 128x128, 1024 envs/GPU"},
+}
 
 
 # ------------------------------------------------------------------------------ helpers
@@ -64,6 +80,7 @@ class ClockSampler:
     def __init__(self, gpu_index):
         self.idx = gpu_index
         self.proc = None
+        self.out = ""
 
     def __enter__(self):
         try:
@@ -77,7 +94,6 @@ class ClockSampler:
 
     def __exit__(self, *exc):
         time.sleep(0.25)
-        self.out = ""
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -104,11 +120,12 @@ class ClockSampler:
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": rows[0][1], "reasons": reasons, "samples": len(rows)}
 
 
-def algorithmic_bytes_per_env_step(scene, obs_dim, action_dim):
-    """Bytes the fused step must move per env-step: action read,
-    articulation + actor state read and written, drive-target write, goal read/write, obs
-    and reward write, flags and counters.  Scratch (link poses, contact rows) is on-chip and
-    the link-pose cache write counts as output."""
+def sim_bytes_per_env_step(scene, obs_dim, action_dim):
+    """Bytes the fused step must move per env-step.
+
+    Counted: the action read; articulation and actor state read and written; the drive-target
+    write; goal read/write; obs and reward writes; flags and counters. Scratch (link poses,
+    contact rows) is on-chip; the link-pose cache write counts as output."""
     D, A, L = scene.models[0].D, scene.models[0].A, scene.models[0].L
     f8 = 8
     b = 4 * action_dim                       # action (f32)
@@ -123,11 +140,24 @@ def algorithmic_bytes_per_env_step(scene, obs_dim, action_dim):
     return b
 
 
+def render_bytes_per_env_step(renderer, scene):
+    """Frame bytes written per env-step: rgb 3 + depth 4 + seg 2 per pixel (+ pointcloud 24),
+    plus the state read the rasterizer needs (link-pose cache, actor poses, camera pose)."""
+    b = 0
+    for g in renderer.groups:
+        px = g["w"] * g["h"] * len(g["cams"])
+        b += px * (3 + 4 + 2) + (px * 24 if g["pc"] is not None else 0)
+        b += len(g["cams"]) * (7 * 8 + 4 * 4)
+    m = scene.models[0]
+    b += (m.L + m.A) * 7 * 8
+    return b
+
+
 # ------------------------------------------------------------------------------ CPU path
 def _cpu_worker(args):
     """One host process: the oracle (numpy restatement of the reference path) on a slice of
     envs.  Runs `warmup` steps, waits on the barrier, then `steps` steps (or `seconds`)."""
-    (rank, n_envs, env_offset, seed, warmup, steps, seconds, barrier, q) = args
+    (rank, n_envs, env_offset, seed, warmup, steps, seconds, obs_mode, barrier, q) = args
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     os.environ["OMP_NUM_THREADS"] = "1"
     import numpy as np
@@ -139,13 +169,41 @@ def _cpu_worker(args):
     spec = PickCubeSpec()
     orc = PickCubeOracle(spec, pickcube_desc(spec), n_envs, seed, env_offset=env_offset)
     ids = np.arange(env_offset, env_offset + n_envs)
-    for k in range(warmup):
+    render = None
+    if obs_mode != "state":
+        from oracle import raster
+        from oracle.contacts import shape_world_poses
+        from paper_2410_00425_b200 import meshes
+        from paper_2410_00425_b200.cameras import RenderParams, default_cameras
+
+        m = orc.model
+        kinds = {0: "sphere", 1: "box", 2: "capsule", 3: "cylinder", 4: "plane"}
+        mesh = meshes.model_mesh([{"kind": kinds[int(m.s_kind[s])], "size": tuple(m.s_size[s])} for s in range(m.S)])
+        cam = default_cameras()[0]
+        rp = RenderParams()
+        L = np.asarray(rp.light_dir) / np.linalg.norm(rp.light_dir)
+        colors = m.s_color[:, :3].astype(np.float32)
+
+        def render():
+            LP, LQ = orc.link_poses()
+            SP, SQ = shape_world_poses(m, LP, LQ, orc.st.ap, orc.st.aq)
+            for e in range(n_envs):
+                raster.render_frame(mesh, m.s_seg, SP[e], SQ[e], np.asarray(cam.pose_p), np.asarray(cam.pose_q),
+                                    (cam.fx, cam.fy, cam.cx, cam.cy), cam.width, cam.height, cam.near, cam.far,
+                                    colors, L, rp.ambient, rp.diffuse, rp.background, obs_mode == "pointcloud")
+
+    def one(k):
         orc.step(action_uniforms(seed, k, ids, 3))
+        if render is not None:
+            render()
+
+    for k in range(warmup):
+        one(k)
     barrier.wait()
     t0 = time.perf_counter()
     k = 0
     while True:
-        orc.step(action_uniforms(seed, warmup + k, ids, 3))
+        one(warmup + k)
         k += 1
         if steps is not None and k >= steps:
             break
@@ -154,7 +212,7 @@ def _cpu_worker(args):
     q.put((rank, k, n_envs, time.perf_counter() - t0))
 
 
-def cpu_reference(total_envs, warmup, steps=None, seconds=None, seed=0):
+def cpu_reference(total_envs, warmup, steps=None, seconds=None, seed=0, obs_mode="state"):
     """Time the CPU path with one process per host core.  Returns (env-steps/s, cores, info)."""
     import multiprocessing as mp
 
@@ -165,7 +223,8 @@ def cpu_reference(total_envs, warmup, steps=None, seconds=None, seed=0):
     q = ctx.Queue()
     per = [total_envs // procs + (1 if r < total_envs % procs else 0) for r in range(procs)]
     offs = [sum(per[:r]) for r in range(procs)]
-    ps = [ctx.Process(target=_cpu_worker, args=((r, per[r], offs[r], seed, warmup, steps, seconds, barrier, q),))
+    ps = [ctx.Process(target=_cpu_worker,
+                      args=((r, per[r], offs[r], seed, warmup, steps, seconds, obs_mode, barrier, q),))
           for r in range(procs)]
     for p in ps:
         p.start()
@@ -187,15 +246,17 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    total = ENVS_PER_GPU * args.gpus
-    rate, cores, info = cpu_reference(total, args.warmup, steps=args.steps, seed=args.seed)
+    wl = WORKLOADS[args.config]
+    total = wl["envs"] * args.gpus
+    rate, cores, info = cpu_reference(total, args.warmup, steps=args.steps, seed=args.seed, obs_mode=wl["obs_mode"])
     ms = total / rate * 1e3
     line = {"metric": METRIC, "value": rate, "unit": "env-steps/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (Philox-seeded resets and actions)",
             "impl": "reference",
-            "config": {"workload": WORKLOAD.replace("4096 envs/GPU", f"{total} envs"), "num_envs": total,
-                       "sim_freq": 120, "control_freq": 60, "solver_pos_iters": 4, "solver_vel_iters": 0},
+            "config": {"workload": wl["desc"].replace(f"{wl['envs']} envs/GPU", f"{total} envs"),
+                       "num_envs": total, "sim_freq": 120, "control_freq": 60, "solver_pos_iters": 4,
+                       "solver_vel_iters": 0},
             "cpu_baseline": {"value": rate, "unit": "env-steps/s", "cores": cores, "kind": "port",
                              "sample": info},
             "e2e": {"value": rate, "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -204,20 +265,161 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------------------ GPU path
+def measure(env, steps, warmup, flush, dist, local, seed_step=0):
+    """Device timing of `steps` env steps: per step, flush L2 (untimed), then events around
+    the random-action launch, the fused step and the render."""
+    import torch
+
+    stream = torch.cuda.current_stream(env.device)
+    for k in range(warmup):
+        env.step_random(seed_step + k)
+    torch.cuda.synchronize()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(steps):
+            flush.zero_()                      # cold L2 before every timed step (not timed)
+            ev[k][0].record(stream)
+            env.random_actions(seed_step + warmup + k)
+            ev[k][1].record(stream)
+            env._launch_sim(env.action_buf.data_ptr())
+            ev[k][2].record(stream)
+            env._render()
+            ev[k][3].record(stream)
+        torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t = torch.tensor([sum(e[0].elapsed_time(e[3]) for e in ev), sum(e[1].elapsed_time(e[2]) for e in ev),
+                      sum(e[2].elapsed_time(e[3]) for e in ev)], dtype=torch.float64, device=env.device)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    launches = 2 + (len(env.renderer.groups) if env.renderer is not None else 0)
+    return {"step_ms": float(t[0]), "sim_ms": float(t[1]), "render_ms": float(t[2]), "clocks": clk.summary(),
+            "launches": launches * steps}
+
+
+def measure_e2e(env, steps, dist, seed):
+    """The public API with host buffers: Env.step(pinned host action) + D2H of obs and reward."""
+    import numpy as np
+    import torch
+
+    N = env.num_envs
+    stream = torch.cuda.current_stream(env.device)
+    rng = np.random.default_rng(seed)
+    host_actions = torch.from_numpy(rng.uniform(-1, 1, (steps, N, env.action_dim)).astype(np.float32)).pin_memory()
+    obs0 = env.step(host_actions[0]).obs
+    flat = {"state": obs0} if not isinstance(obs0, dict) else _flatten(obs0)
+    hosts = {k: torch.empty(v.shape, dtype=v.dtype).pin_memory() for k, v in flat.items()}
+    rew_host = torch.empty((N,), dtype=torch.float32).pin_memory()
+    d2h = sum(v.numel() * v.element_size() for v in flat.values()) + N * 4
+    env.capture_graph()
+    for k in range(3):
+        env.step(host_actions[k])
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for k in range(steps):
+        r = env.step(host_actions[k])                 # H2D of the action inside
+        cur = {"state": r.obs} if not isinstance(r.obs, dict) else _flatten(r.obs)
+        for name, v in cur.items():
+            hosts[name].copy_(v, non_blocking=True)   # D2H of the step's results
+        rew_host.copy_(r.reward, non_blocking=True)
+        stream.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if dist is not None:
+        tt = torch.tensor([e2e_s], dtype=torch.float64, device=env.device)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt[0])
+    return e2e_s, N * env.action_dim * 4, d2h
+
+
+def _flatten(d, prefix=""):
+    out = {}
+    for k, v in d.items():
+        if isinstance(v, dict):
+            out.update(_flatten(v, prefix + k + "/"))
+        else:
+            out[prefix + k] = v
+    return out
+
+
+def run_workload(name, steps, warmup, world, rank, local, dist, flush, seed, e2e_steps, cpu):
+    import torch
+
+    from paper_2410_00425_b200.tasks import make_task
+
+    wl = WORKLOADS[name]
+    n_global = wl["envs"] * world
+    env = make_task("PickCube", n_global, seed=seed, obs_mode=wl["obs_mode"],
+                    shard=(rank, world) if world > 1 else None)
+    N = env.num_envs
+    m = measure(env, steps, warmup, flush, dist, local)
+    value = n_global * steps / (m["step_ms"] / 1e3)
+    stats = torch.stack([env.success.sum().double(), env.terminated.sum().double(), env.truncated.sum().double()])
+    if dist is not None:
+        dist.all_reduce(stats)  # rollout statistics: the only data collective
+    e2e_s, h2d, d2h = measure_e2e(env, e2e_steps, dist, seed + rank)
+    e2e = {"value": n_global * e2e_steps / e2e_s, "unit": "env-steps/s", "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+           "path": "Env.step(pinned host action) + every obs tensor and the reward D2H, CUDA graph"}
+    peak, peak_kind = _peaks()
+    sim_b = sim_bytes_per_env_step(env.scene, env.obs_dim, env.action_dim)
+    sim_s = m["sim_ms"] / 1e3 / steps
+    kernels = {"k_step": {"us_per_launch": sim_s * 1e6, "bytes_per_env_step": sim_b,
+                          "achieved_gbs": sim_b * N / sim_s / 1e9}}
+    dominant = "k_step"
+    if env.renderer is not None:
+        rb = render_bytes_per_env_step(env.renderer, env.scene)
+        rs = m["render_ms"] / 1e3 / steps
+        kernels["k_render"] = {"us_per_launch": rs * 1e6, "bytes_per_env_step": rb, "achieved_gbs": rb * N / rs / 1e9}
+        if rs > sim_s:
+            dominant = "k_render"
+    dk = kernels[dominant]
+    roof = {"bound": "hbm", "achieved": dk["achieved_gbs"], "peak": peak, "unit": "GB/s",
+            "frac": dk["achieved_gbs"] / peak, "traffic": None, "kernel": dominant,
+            "bytes_per_env_step": dk["bytes_per_env_step"], "kernel_us_per_launch": dk["us_per_launch"],
+            "peak_source": peak_kind, "kernels": kernels}
+    line = {"metric": METRIC, "value": value, "unit": "env-steps/s", "n_gpus": world, "steps": steps,
+            "warmup": warmup, "ms_per_step": m["step_ms"] / steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (Philox-seeded resets and device-generated uniform actions)",
+            "config": {"workload": wl["desc"], "num_envs_per_gpu": wl["envs"], "global_envs": n_global,
+                       "obs_mode": wl["obs_mode"], "sim_freq": 120, "control_freq": 60, "solver_pos_iters": 4,
+                       "solver_vel_iters": 0, "parallelism": f"env-shard x{world}",
+                       "l2": "flushed (256 MiB write) before each timed step"},
+            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": m["clocks"],
+            "gpu_launches": m["launches"],
+            "rollout_stats": {"success": float(stats[0]), "terminated": float(stats[1]), "truncated": float(stats[2])}}
+    del env
+    torch.cuda.empty_cache()
+    return line
+
+
 def run_ours(args):
     import torch
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        if world == 1 and args.gpus > 1:
-            raise SystemExit("--gpus N>1 must be launched with torch.distributed.run (one rank per GPU)")
-    # CPU baseline first (before CUDA is initialised in this process; spawn-based workers)
-    cpu = None
+    if world == 1 and args.gpus > 1:
+        raise SystemExit("--gpus N>1 must be launched with torch.distributed.run (one rank per GPU)")
+    # CPU baselines first (before CUDA is initialised in this process; spawn-based workers)
+    cpu, cpu2 = None, None
     if rank == 0 and world == 1 and not args.no_cpu:
-        rate, cores, info = cpu_reference(ENVS_PER_GPU, 2, seconds=args.cpu_seconds, seed=args.seed)
+        wl = WORKLOADS[args.config]
+        rate, cores, info = cpu_reference(wl["envs"], 2, seconds=args.cpu_seconds, seed=args.seed,
+                                          obs_mode=wl["obs_mode"])
         cpu = {"value": rate, "unit": "env-steps/s", "cores": cores, "kind": "port", "sample": info}
+        if args.secondary:
+            w2 = WORKLOADS[args.secondary]
+            n2 = 4 * len(os.sched_getaffinity(0))  # bounded sample: 4 envs per core
+            rate, cores, info = cpu_reference(n2, 1, seconds=args.cpu_seconds / 2, seed=args.seed,
+                                              obs_mode=w2["obs_mode"])
+            cpu2 = {"value": rate, "unit": "env-steps/s", "cores": cores, "kind": "port", "sample": info}
 
     torch.cuda.set_device(local)
     dist = None
@@ -226,99 +428,17 @@ def run_ours(args):
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2410_00425_b200 import _native as nat
-    from paper_2410_00425_b200.tasks import make_task
 
     nat.ensure_device(local)
-    n_global = ENVS_PER_GPU * world
-    env = make_task("PickCube", n_global, seed=args.seed, shard=(rank, world) if world > 1 else None)
-    N = env.num_envs
-    dev = env.device
-    stream = torch.cuda.current_stream(dev)
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-
-    # ---------------- device-resident throughput (`value`) + step-kernel time (`roofline`)
-    for k in range(args.warmup):
-        env.step_random(k)
-    torch.cuda.synchronize()
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    if dist is not None:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        for k in range(args.steps):
-            flush.zero_()                      # cold L2 before every timed step (not timed)
-            ev[k][0].record(stream)
-            env.random_actions(args.warmup + k)
-            ev[k][1].record(stream)
-            env.launch_step()
-            ev[k][2].record(stream)
-        torch.cuda.synchronize()
-    if dist is not None:
-        dist.barrier()
-    torch.cuda.synchronize()
-    step_ms = sum(e[0].elapsed_time(e[2]) for e in ev)
-    kern_ms = sum(e[1].elapsed_time(e[2]) for e in ev)
-    t = torch.tensor([step_ms, kern_ms], dtype=torch.float64, device=dev)
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    step_ms, kern_ms = float(t[0]), float(t[1])
-    value = n_global * args.steps / (step_ms / 1e3)
-
-    # rollout statistics: the only collective (NCCL all-reduce of a few scalars)
-    stats = torch.stack([env.success.sum().double(), env.terminated.sum().double(),
-                         env.truncated.sum().double(), env.reward.double().sum()])
-    if dist is not None:
-        dist.all_reduce(stats)
-
-    # ---------------- end to end through the public API with host buffers (`e2e`)
-    import numpy as np
-
-    e2e_steps = max(args.steps, 20)
-    rng = np.random.default_rng(args.seed + rank)
-    host_actions = torch.from_numpy(rng.uniform(-1, 1, (e2e_steps, N, env.action_dim)).astype(np.float32))
-    host_actions = host_actions.pin_memory()
-    obs_host = torch.empty((N, env.obs_dim), dtype=torch.float32).pin_memory()
-    rew_host = torch.empty((N,), dtype=torch.float32).pin_memory()
-    env.capture_graph()
-    for k in range(3):
-        r = env.step(host_actions[k])
-    torch.cuda.synchronize()
-    if dist is not None:
-        dist.barrier()
-    t0 = time.perf_counter()
-    for k in range(e2e_steps):
-        r = env.step(host_actions[k])                 # H2D of the action inside
-        obs_host.copy_(r.obs, non_blocking=True)      # D2H of the step's results
-        rew_host.copy_(r.reward, non_blocking=True)
-        stream.synchronize()
-    e2e_s = time.perf_counter() - t0
-    if dist is not None:
-        tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_s = float(tt[0])
-    e2e = {"value": n_global * e2e_steps / e2e_s, "unit": "env-steps/s",
-           "h2d_bytes_per_step": N * env.action_dim * 4, "d2h_bytes_per_step": N * (env.obs_dim + 1) * 4,
-           "steps": e2e_steps, "path": "Env.step(pinned host action) + obs/reward D2H, CUDA graph"}
-
-    peak, peak_kind = _peaks()
-    bpe = algorithmic_bytes_per_env_step(env.scene, env.obs_dim, env.action_dim)
-    kern_s = kern_ms / 1e3 / args.steps
-    achieved = bpe * N / kern_s / 1e9
-    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": None, "kernel": "k_step (fused step)", "bytes_per_env_step": bpe,
-            "kernel_us_per_launch": kern_s * 1e6, "peak_source": peak_kind}
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=torch.device("cuda", local))
+    line = run_workload(args.config, args.steps, args.warmup, world, rank, local, dist, flush, args.seed,
+                        max(args.steps, 20), cpu)
+    if args.secondary:
+        sec = run_workload(args.secondary, max(args.steps // 4, 20), max(args.warmup, 3), world, rank, local, dist,
+                           flush, args.seed, 20, cpu2)
+        line["secondary"] = {k: sec[k] for k in ("value", "unit", "ms_per_step", "steps", "config", "e2e", "roofline",
+                                                 "cpu_baseline", "clocks", "gpu_launches")}
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": "env-steps/s", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": step_ms / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (Philox-seeded resets and device-generated uniform actions)",
-                "config": {"workload": WORKLOAD, "num_envs_per_gpu": ENVS_PER_GPU, "global_envs": n_global,
-                           "sim_freq": 120, "control_freq": 60, "solver_pos_iters": 4, "solver_vel_iters": 0,
-                           "parallelism": f"env-shard x{world}", "l2": "flushed (256 MiB write) before each timed step"},
-                "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary(),
-                "gpu_launches": 2 * args.steps,
-                "rollout_stats": {"success": float(stats[0]), "terminated": float(stats[1]),
-                                  "truncated": float(stats[2])}}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
@@ -331,12 +451,16 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", choices=sorted(WORKLOADS), default="c2")
+    ap.add_argument("--secondary", default="c3", help="extra workload measured after the headline ('' = none)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline legs")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    if args.secondary == args.config:
+        args.secondary = ""
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

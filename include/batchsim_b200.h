@@ -34,7 +34,7 @@ extern "C" {
 #define BS_ERR_UNSUPPORTED 6 /* ModelError      (errors.py:40) */
 
 /* ABI version: bumped whenever a signature or a struct layout below changes. */
-#define BS_ABI_VERSION 1
+#define BS_ABI_VERSION 2
 int bs_abi_version(void);
 
 /* Bind the library's CUDA runtime to `device` (call once per process/thread before use;
@@ -132,6 +132,7 @@ typedef struct BsModelTables {
   const int32_t* pair_i;       /* [M][P_max] first shape slot (body A)           */
   const int32_t* pair_j;       /* [M][P_max] second shape slot (body B)          */
   const int32_t* pair_code;    /* [M][P_max] BS_PAIR_* (| BS_PAIR_SWAP)          */
+  const int32_t* pair_slot;    /* [M][P_max] first contact slot of the pair (prefix of max contacts) */
   const double* actor_mass;    /* [M][A_max] */
   const double* actor_inertia; /* [M][A_max][3] principal, body frame            */
 } BsModelTables;

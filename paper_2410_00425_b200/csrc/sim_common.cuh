@@ -88,7 +88,7 @@ struct Model {
   const int32_t* ctrl;
   const int32_t *s_btype, *s_body, *s_kind, *s_seg;
   const R *s_size, *s_frame, *s_radius;
-  const int32_t *p_i, *p_j, *p_code;
+  const int32_t *p_i, *p_j, *p_code, *p_slot;
   const R *a_mass, *a_inertia;
 };
 
@@ -105,7 +105,7 @@ __device__ __forceinline__ Model model_of(const BsModelTables& T, int m) {
   M.s_btype = T.shape_btype + so; M.s_body = T.shape_body + so; M.s_kind = T.shape_kind + so;
   M.s_seg = T.shape_seg + so; M.s_size = T.shape_size + 3 * so; M.s_frame = T.shape_frame + 7 * so;
   M.s_radius = T.shape_radius + so;
-  M.p_i = T.pair_i + po; M.p_j = T.pair_j + po; M.p_code = T.pair_code + po;
+  M.p_i = T.pair_i + po; M.p_j = T.pair_j + po; M.p_code = T.pair_code + po; M.p_slot = T.pair_slot + po;
   M.a_mass = T.actor_mass + ao; M.a_inertia = T.actor_inertia + 3 * ao;
   return M;
 }

@@ -35,7 +35,7 @@ using namespace bs::sim;
 struct Lay {
   int Dm, Lm, Sm, Cm, Am, NU, RW, KCH;
   int q, qd, tgt, apose, avel, goal;
-  int lpq, Sv, In, Mt, Minv, cb, uq, uv, uw, Iwi, spq;
+  int lpq, Sv, In, Mt, Minv, cb, u, Iwi, spq;
   int Tl, V, Ac, F, ct, rows;
   int total;
 };
@@ -321,6 +321,8 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
   //         motion (gyroscopic + gravity), zero the mass matrix
   const V3<R> grav = v3(P.gravity[0], P.gravity[1], P.gravity[2]);
   for (int i = l; i < D * Dm; i += G) Mt[i] = 0.0;
+  for (int i = D + l; i < Dm; i += G) E[Y.u + i] = 0.0;
+  for (int i = Dm + 6 * A + l; i < Y.NU; i += G) E[Y.u + i] = 0.0;
   for (int t = l; t < L + NS + A; t += G) {
     if (t < L) {
       const int k = t, jt = M.jtype[k];
@@ -351,8 +353,8 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
       R Iw[9], Iwi[9];
       actor_inertia_f(M.a_inertia + 3 * a, aq, Iw, Iwi);
       V3<R> gyro = scl(crs(aw, m3mul(Iw, aw)), -1.0);
-      st3(E + Y.uw + 3 * a, add(aw, scl(m3mul(Iwi, gyro), dt)));
-      st3(E + Y.uv + 3 * a, add(av, scl(grav, dt)));
+      st3(E + Y.u + Dm + 6 * a, add(av, scl(grav, dt)));
+      st3(E + Y.u + Dm + 6 * a + 3, add(aw, scl(m3mul(Iwi, gyro), dt)));
 #pragma unroll
       for (int j = 0; j < 9; ++j) E[Y.Iwi + 9 * a + j] = Iwi[j];
     }
@@ -469,7 +471,7 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
     } else {
 #pragma unroll
       for (int i = 0; i < MD; ++i)
-        if (i < D) E[Y.uq + i] = E[Y.qd + i] + dt * x[i];
+        if (i < D) E[Y.u + i] = E[Y.qd + i] + dt * x[i];
     }
   }
   // ---- H: broadphase + narrowphase into fixed per-pair candidate slots (A-5)
@@ -479,9 +481,7 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
   __syncwarp();
   int unsup = 0;
   for (int pi = l; pi < M.P; pi += G) {
-    int base = 0;
-    for (int q2 = 0; q2 < pi; ++q2) base += pair_maxc(M.p_code[q2]);
-    unsup += narrow_pair(M, pi, spq, slop, cand + 8 * base);
+    unsup += narrow_pair(M, pi, spq, slop, cand + 8 * M.p_slot[pi]);
   }
 #pragma unroll
   for (int o = G / 2; o > 0; o >>= 1) unsup += __shfl_xor_sync(FULLMASK, unsup, o);
@@ -568,25 +568,23 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
   }
   __syncwarp();
 
-  // ---- K: projected Gauss-Seidel, sequential row order, executed by every
-  //         lane of the group on a register copy of u (identical in every lane afterwards)
-  constexpr int NUM = K::NU;
-  R u[NUM];
+  // ---- K: projected Gauss-Seidel, sequential row order.  The velocity
+  //         vector is distributed over the group (lane l owns u[l], u[l+G], ...): each row is a
+  //         lane-local partial dot, a 3-level shuffle all-reduce inside the group, the
+  //         (redundant) multiplier update, and a lane-local axpy.
+  constexpr int NUM = K::NU, KU = (NUM + G - 1) / G;
+  const unsigned gmask = (G == 32 ? FULLMASK : ((1u << G) - 1u)) << (g * G);
+  R u[KU];
 #pragma unroll
-  for (int k = 0; k < NUM; ++k) {
-    R x = 0.0;
-    if (k < Dm) x = k < D ? E[Y.uq + k] : 0.0;
-    else if (k < NU) {
-      const int a = (k - Dm) / 6, j = (k - Dm) - 6 * a;
-      if (a < A) x = j < 3 ? E[Y.uv + 3 * a + j] : E[Y.uw + 3 * a + j - 3];
-    }
-    u[k] = x;
+  for (int j = 0; j < KU; ++j) {
+    const int k = l + G * j;
+    u[j] = k < NU ? E[Y.u + k] : 0.0;
   }
   const int iters = P.pos_iters + P.vel_iters;
   const R mu = P.friction;
   for (int it = 0; it < iters; ++it) {
     const bool pos_phase = it < P.pos_iters;
-    const R* row = rows;
+    R* row = rows;
     for (int c = 0; c < nc; ++c) {
       R lam_n = 0.0;
 #pragma unroll
@@ -599,13 +597,14 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
         }
         const R* J = row + ROW_J;
         const R* Wr = J + NU;
-        R v0 = 0.0, v1 = 0.0;  // two partial sums for ILP
+        R v = 0.0;
 #pragma unroll
-        for (int k = 0; k < NUM; k += 2) {
-          if (k < NU) v0 += J[k] * u[k];
-          if (k + 1 < NUM && k + 1 < NU) v1 += J[k + 1] * u[k + 1];
+        for (int j = 0; j < KU; ++j) {
+          const int k = l + G * j;
+          if (k < NU) v += J[k] * u[j];
         }
-        const R v = v0 + v1;
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(gmask, v, o);
         R nw;
         if (rr == 0) {
           const R tgt = pos_phase ? row[2] : row[3];
@@ -616,24 +615,33 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
           nw = fmin(fmax(old + (0.0 - v) * invK, -bound), bound);
         }
         const R delta = nw - old;
-        const_cast<R*>(row)[1] = nw;  // every lane stores the same value and reads back its own
+        row[1] = nw;  // every lane stores the same value and reads back its own
 #pragma unroll
-        for (int k = 0; k < NUM; ++k)
-          if (k < NU) u[k] += delta * Wr[k];
+        for (int j = 0; j < KU; ++j) {
+          const int k = l + G * j;
+          if (k < NU) u[j] += delta * Wr[k];
+        }
       }
     }
   }
+#pragma unroll
+  for (int j = 0; j < KU; ++j) {
+    const int k = l + G * j;
+    if (k < NU) E[Y.u + k] = u[j];
+  }
+  __syncwarp();
 
   // ---- L: semi-implicit Euler, joint limits (A-7), actor orientation (A-8), divergence
-  //         freeze.  Every lane holds the same velocities, so every lane
-  //         evaluates the update; lanes then write disjoint entries.
+  //         freeze.  Every lane evaluates the (small) update from the
+  //         shared u; lanes then write disjoint entries.
   R q1[MD], qd1[MD];
   bool finite = true;
 #pragma unroll
   for (int i = 0; i < MD; ++i) {
     if (i < D) {
-      R v = E[Y.q + i] + dt * u[i];
-      R w = u[i];
+      const R ui = E[Y.u + i];
+      R v = E[Y.q + i] + dt * ui;
+      R w = ui;
       const R lo = M.lower[i], hi = M.upper[i];
       if (v < lo) { v = lo; w = fmax(w, 0.0); }
       else if (v > hi) { v = hi; w = fmin(w, 0.0); }
@@ -647,16 +655,9 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
 #pragma unroll
   for (int a = 0; a < MA; ++a) {
     if (a < A) {
-      // u index of actor a's block: Dm + 6a (Dm may be < MD, so select at run time)
       R blk[6];
 #pragma unroll
-      for (int j = 0; j < 6; ++j) {
-        R x = 0.0;
-#pragma unroll
-        for (int k = 0; k < NUM; ++k)
-          if (k == Dm + 6 * a + j) x = u[k];
-        blk[j] = x;
-      }
+      for (int j = 0; j < 6; ++j) blk[j] = E[Y.u + Dm + 6 * a + j];
       uva[a] = v3(blk[0], blk[1], blk[2]);
       uwa[a] = v3(blk[3], blk[4], blk[5]);
       const V3<R> ap = ld3(E + Y.apose + 7 * a);
@@ -860,9 +861,7 @@ static Lay make_lay(const BsModelTables& T, int G) {
   y.Mt = o; o += y.Dm * y.Dm;
   y.Minv = o; o += y.Dm * y.Dm;
   y.cb = o; o += y.Dm;
-  y.uq = o; o += y.Dm;
-  y.uv = o; o += 3 * y.Am;
-  y.uw = o; o += 3 * y.Am;
+  y.u = o; o += y.Dm + 6 * y.Am;
   y.Iwi = o; o += 9 * y.Am;
   y.spq = o; o += 7 * y.Sm;
   // union: {FK local transforms + RNEA temporaries} | {compacted contacts}
@@ -882,13 +881,13 @@ static int launch(const BsModelTables& T, const BsEnvState& S, const BsStepOutpu
                   const float* action, cudaStream_t st) {
   const Lay y = make_lay(T, K::G);
   const size_t bytes = (size_t)K::EPW * y.total * sizeof(double);
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(k_step<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
+  if (bytes > 220 * 1024) return BS_ERR_UNSUPPORTED;
+  static size_t attr_bytes = 0;  // opt-in above 48 KB, raised on demand
+  if (bytes > attr_bytes) {
+    if (cudaFuncSetAttribute(k_step<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
       return BS_ERR_CUDA;
-    attr_set = true;
+    attr_bytes = bytes;
   }
-  if (bytes > 227 * 1024) return BS_ERR_UNSUPPORTED;
   const int blocks = (S.num_envs + K::EPW - 1) / K::EPW;
   k_step<K><<<blocks, 32, bytes, st>>>(T, S, O, P, action, y);
   return launch_status();

@@ -139,9 +139,12 @@ class Env:
         self._render()
         return self._obs()
 
-    def _launch_step(self, action_ptr):
+    def _launch_sim(self, action_ptr):
         nat.call("bs_step", ctypes.byref(self.scene.c_tables), ctypes.byref(self.scene.c_state),
                  ctypes.byref(self.c_out), ctypes.byref(self.c_params), action_ptr, nat.stream_handle())
+
+    def _launch_step(self, action_ptr):
+        self._launch_sim(action_ptr)
         self._render()
 
     def _render(self):

@@ -236,7 +236,7 @@ class SceneBatch:
             ("shape_body", (M, Sm), i32), ("shape_kind", (M, Sm), i32), ("shape_seg", (M, Sm), i32),
             ("shape_size", (M, Sm, 3), f64), ("shape_frame", (M, Sm, 7), f64), ("shape_radius", (M, Sm), f64),
             ("shape_color", (M, Sm, 4), np.float32), ("pair_i", (M, Pm), i32), ("pair_j", (M, Pm), i32),
-            ("pair_code", (M, Pm), i32), ("actor_mass", (M, Am), f64), ("actor_inertia", (M, Am, 3), f64)]}
+            ("pair_code", (M, Pm), i32), ("pair_slot", (M, Pm), i32), ("actor_mass", (M, Am), f64), ("actor_inertia", (M, Am, 3), f64)]}
         t["link_parent"][:] = -2
         t["link_dof"][:] = -1
         t["dof_ctrl"][:] = -1
@@ -270,8 +270,11 @@ class SceneBatch:
                 t["shape_frame"][m, s] = (*sh["p"], *sh["q"])
                 t["shape_radius"][m, s] = _bounding_radius(sh["kind"], sh["size"])
                 t["shape_color"][m, s] = sh["color"]
+            slot = 0
             for p, (i, j, code) in enumerate(pm.pairs):
                 t["pair_i"][m, p], t["pair_j"][m, p], t["pair_code"][m, p] = i, j, code
+                t["pair_slot"][m, p] = slot
+                slot += cabi.PAIR_MAXC.get(code & 15, 0)
             for a, (mass, inertia) in enumerate(pm.actors):
                 t["actor_mass"][m, a] = mass
                 t["actor_inertia"][m, a] = inertia

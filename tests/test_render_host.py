@@ -4,7 +4,7 @@ import numpy as np
 
 
 def test_randomize_cameras_properties():
-    from paper_2410_00425_b200.render import CameraJitter, default_cameras, randomize_cameras
+    from paper_2410_00425_b200.cameras import CameraJitter, default_cameras, randomize_cameras
 
     cams = default_cameras()
     p0, k0 = randomize_cameras(cams, 4, 7, CameraJitter())

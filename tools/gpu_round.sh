@@ -1,13 +1,14 @@
 #!/bin/bash
-# One GPU session: GPU tests, bench (ours + reference arm), launch list, ncu capture of the
-# step kernel.  Usage (under gpurun): bash tools/gpu_round.sh [tag] [skip-ref]
+# One GPU session: GPU tests, bench (ours + reference arm), launch list, ncu captures of the
+# step and render kernels.  Usage (under gpurun): bash tools/gpu_round.sh [tag] [skip-ref]
 cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
 TAG=${1:-run}
 timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/${TAG}_gpu_tests.log 2>&1; echo "exit $?" >> gpurun_out/${TAG}_gpu_tests.log
-timeout 400 python bench.py --steps 200 --warmup 10 > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
+timeout 600 python bench.py --steps 200 --warmup 10 > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
 if [ "$2" != "skip-ref" ]; then
   timeout 300 python bench.py --steps 50 --warmup 5 --impl reference > gpurun_out/${TAG}_bench_ref.json 2>> gpurun_out/${TAG}_bench.err
 fi
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 5 --warmup 3 --no-cpu > /dev/null 2>> gpurun_out/${TAG}_ncu.err
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_step -s 3 -c 2 -o gpurun_out/${TAG}_prof_step python bench.py --steps 3 --warmup 3 --no-cpu > /dev/null 2>> gpurun_out/${TAG}_ncu.err
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_step -s 3 -c 1 -o gpurun_out/${TAG}_prof_step python bench.py --steps 3 --warmup 3 --no-cpu --secondary "" > /dev/null 2>> gpurun_out/${TAG}_ncu.err
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_render -s 3 -c 1 -o gpurun_out/${TAG}_prof_render python bench.py --config c3 --steps 3 --warmup 3 --no-cpu --secondary "" > /dev/null 2>> gpurun_out/${TAG}_ncu.err
 echo done
