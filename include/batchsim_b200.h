@@ -34,7 +34,7 @@ extern "C" {
 #define BS_ERR_UNSUPPORTED 6 /* ModelError      (errors.py:40) */
 
 /* ABI version: bumped whenever a signature or a struct layout below changes. */
-#define BS_ABI_VERSION 2
+#define BS_ABI_VERSION 3
 int bs_abi_version(void);
 
 /* Bind the library's CUDA runtime to `device` (call once per process/thread before use;
@@ -176,7 +176,8 @@ typedef struct BsSimParams {
   double friction, beta, slop;
   int32_t ctrl_mode;           /* BS_CTRL_*                                      */
   int32_t action_dim;
-  double action_scale;
+  double action_scale;         /* joint modes: rad (or m) per unit action; ee mode: m */
+  double action_scale_rot;     /* pd_ee_delta_pose: rad per unit rotation action   */
   double ik_lambda;
   int32_t ee_link;             /* controller / task end-effector link index      */
   int32_t task;                /* BS_TASK_*                                      */

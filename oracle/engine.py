@@ -19,8 +19,8 @@ import numpy as np
 
 from . import se3
 from .contacts import detect_contacts, shape_world_poses, tangent_basis
-from .dynamics import (aba, crba, cross, dot, forward_kinematics, link_velocities,
-                       link_world_inertia, motion_subspace, point_jacobian, rnea_bias)
+from .dynamics import (aba, crba, cross, dot, forward_kinematics, geometric_jacobian, ik_delta,
+                       link_velocities, link_world_inertia, motion_subspace, point_jacobian, rnea_bias)
 from .model import BODY_ACTOR, BODY_LINK
 
 
@@ -218,7 +218,10 @@ PD_JOINT_POS, PD_JOINT_DELTA_POS, PD_EE_DELTA_POSE = "pd_joint_pos", "pd_joint_d
 
 def controller_targets(model, ctrl, q, action):
     """SPEC.md:402-410.  ctrl: mode, dofs (controlled dof indices), scale; returns (B, D)
-    targets (uncontrolled dofs keep target = current q, with kp = 0 they are undriven)."""
+    targets (uncontrolled dofs keep target = current q, with kp = 0 they are undriven).
+    pd_ee_delta_pose: twist = (a[0:3] * scale m, a[3:6] * rot_scale rad),
+    world frame, at the ee link origin; dq = J^T (J J^T + lam^2 I)^-1 twist over the controlled
+    columns of the geometric Jacobian; target = clamp(q + dq)."""
     a = np.clip(np.asarray(action, np.float64), -1.0, 1.0)
     tgt = q.copy()
     dofs = np.asarray(ctrl.dofs)
@@ -229,6 +232,13 @@ def controller_targets(model, ctrl, q, action):
         span_ok = np.isfinite(lo) & np.isfinite(hi)
         un = np.where(span_ok, lo + (a + 1.0) * 0.5 * (hi - lo), a * ctrl.scale)
         tgt[:, dofs] = np.clip(un, lo, hi)
+    elif ctrl.mode == PD_EE_DELTA_POSE:
+        LP, LQ = forward_kinematics(model, q)
+        S = motion_subspace(model, LP, LQ)
+        J = geometric_jacobian(model, S, ctrl.ee_link, LP[:, ctrl.ee_link])[:, :, dofs]
+        twist = np.concatenate([a[:, :3] * ctrl.scale, a[:, 3:6] * ctrl.rot_scale], -1)
+        dq = ik_delta(J, twist, ctrl.lam)
+        tgt[:, dofs] = np.clip(q[:, dofs] + dq, lo, hi)
     else:
         raise NotImplementedError(ctrl.mode)
     return tgt

@@ -41,7 +41,8 @@ class PickCubeOracle:
         kd = np.full(D, spec.kd)
         self.drv = E.Drives(kp, kd, np.full(D, spec.force_limit), np.zeros((num_envs, D)))
         self.ctrl = type("Ctrl", (), {"mode": spec.control_mode, "dofs": list(range(D)),
-                                      "scale": spec.action_scale})()
+                                      "scale": spec.action_scale, "rot_scale": 0.05, "lam": 0.05,
+                                      "ee_link": self.ee_link})()
         self.reset_count = np.zeros(num_envs, np.uint64)
         self.elapsed = np.zeros(num_envs, np.int32)
         self.goal = np.zeros((num_envs, 3))
@@ -135,3 +136,106 @@ class PickCubeOracle:
         st.av[:], st.aw[:] = snap["av"], snap["aw"]
         self.goal[:] = snap["goal"]
         self.elapsed[:] = snap["elapsed"]
+
+
+class OpenCabinetOracle:
+    """Heterogeneous OpenCabinet (OpenChain-Hetero; A-18): envs are grouped
+    by layout and each group is stepped by the oracle engine (envs are independent,
+    SPEC.md:216).  Reset: arm at q_rest + U(-noise, noise); cabinet parts closed; target part
+    = 3 + floor(u3 * n_parts).  success = q_target > frac * upper; reward = q_target / upper."""
+
+    N_UNIFORMS = 8
+
+    def __init__(self, spec, descs, seed, env_offset=0, cfg=None):
+        self.spec = spec
+        self.cfg = cfg or E.SimConfig()
+        self.B = len(descs)
+        self.seed = seed
+        self.env_ids = np.arange(env_offset, env_offset + self.B, dtype=np.uint64)
+        groups = {}
+        for e, d in enumerate(descs):
+            groups.setdefault(d.key(), (d, []))[1].append(e)
+        self.groups = []
+        for d, idx in groups.values():
+            m = Model(d)
+            D = m.D
+            kp = np.zeros(D)
+            kd = np.zeros(D)
+            fl = np.full(D, np.inf)
+            kp[:3], kd[:3], fl[:3] = spec.kp, spec.kd, spec.force_limit
+            drv = E.Drives(kp, kd, fl, np.zeros((len(idx), D)))
+            ctrl = type("Ctrl", (), {"mode": spec.control_mode, "dofs": [0, 1, 2], "scale": spec.action_scale})()
+            self.groups.append({"model": m, "idx": np.asarray(idx), "drv": drv, "ctrl": ctrl, "st": None,
+                                "ee": m.link_names.index(f"arm/{spec.ee_link}")})
+        self.D_max = max(g["model"].D for g in self.groups)
+        self.reset_count = np.zeros(self.B, np.uint64)
+        self.elapsed = np.zeros(self.B, np.int32)
+        self.target = np.full(self.B, -1, np.int64)
+        self.reset()
+
+    def reset(self, mask=None):
+        s = self.spec
+        for g in self.groups:
+            m, idx = g["model"], g["idx"]
+            sel = np.arange(len(idx)) if mask is None else np.nonzero(mask[idx])[0]
+            if g["st"] is None:
+                B = len(idx)
+                g["st"] = E.State(np.zeros((B, m.D)), np.zeros((B, m.D)), np.zeros((B, 0, 3)),
+                                  np.zeros((B, 0, 4)), np.zeros((B, 0, 3)), np.zeros((B, 0, 3)), np.zeros(B, np.uint8))
+            if not len(sel):
+                continue
+            ge = idx[sel]
+            u = reset_uniforms(self.seed, self.env_ids[ge], self.reset_count[ge], self.N_UNIFORMS)
+            st = g["st"]
+            st.q[sel] = 0.0
+            st.qd[sel] = 0.0
+            for k in range(3):
+                st.q[sel, k] = s.q_rest[k] + uniform(-s.q_noise, s.q_noise, u[:, k])
+            nobj = m.D - 3
+            self.target[ge] = 3 + np.minimum((u[:, 3] * nobj).astype(np.int64), nobj - 1) if nobj > 0 else -1
+            st.diverged[sel] = 0
+            self.elapsed[ge] = 0
+
+    def step(self, action):
+        action = np.asarray(action)
+        reward = np.zeros(self.B, np.float32)
+        success = np.zeros(self.B, bool)
+        fail = np.zeros(self.B, bool)
+        for g in self.groups:
+            m, idx = g["model"], g["idx"]
+            g["st"] = E.control_step(m, g["st"], g["drv"], g["ctrl"], action[idx], self.cfg)
+            t = self.target[idx]
+            rows = np.arange(len(idx))
+            hi = m.upper[t]
+            qv = g["st"].q[rows, t]
+            success[idx] = qv > self.spec.success_frac * hi
+            reward[idx] = (qv / hi).astype(np.float32)
+            fail[idx] = g["st"].diverged != 0
+        self.elapsed += 1
+        terminated = success | fail
+        truncated = self.elapsed >= self.spec.max_steps
+        info = {"success": success, "fail": fail}
+        done = terminated | truncated
+        final = self.snapshot()
+        if done.any():
+            self.reset_count[done] += 1
+            self.reset(done)
+        return reward, terminated, truncated, info, final
+
+    def snapshot(self):
+        q = np.zeros((self.B, self.D_max))
+        qd = np.zeros((self.B, self.D_max))
+        ee = np.zeros((self.B, 3))
+        for g in self.groups:
+            m, idx = g["model"], g["idx"]
+            q[idx, :m.D] = g["st"].q
+            qd[idx, :m.D] = g["st"].qd
+            LP, _ = forward_kinematics(m, g["st"].q)
+            ee[idx] = LP[:, g["ee"]]
+        return {"q": q, "qd": qd, "ee": ee, "target": self.target.copy(), "elapsed": self.elapsed.copy()}
+
+    def load(self, q, qd):
+        for g in self.groups:
+            m, idx = g["model"], g["idx"]
+            g["st"].q[:] = q[idx, :m.D]
+            g["st"].qd[:] = qd[idx, :m.D]

@@ -37,7 +37,7 @@ class BsStepOutputs(ctypes.Structure):
 class BsSimParams(ctypes.Structure):
     _fields_ = [("dt", F64), ("substeps", I32), ("pos_iters", I32), ("vel_iters", I32),
                 ("gravity", F64 * 3), ("friction", F64), ("beta", F64), ("slop", F64),
-                ("ctrl_mode", I32), ("action_dim", I32), ("action_scale", F64), ("ik_lambda", F64),
+                ("ctrl_mode", I32), ("action_dim", I32), ("action_scale", F64), ("action_scale_rot", F64), ("ik_lambda", F64),
                 ("ee_link", I32), ("task", I32), ("max_steps", I32), ("auto_reset", I32),
                 ("early_termination", I32), ("seed", ctypes.c_uint64), ("task_f", F64 * 16)]
 

@@ -714,21 +714,90 @@ __global__ void __launch_bounds__(32) k_step(BsModelTables T, BsEnvState S, BsSt
   if (l < 3) E[Y.goal + l] = S.goal[3 * (int64_t)e + l];
   // ---- controller: drive targets, once per control step
   const float* act = action + (int64_t)e * P.action_dim;
-  for (int i = l; i < M.D; i += G) {
-    const int ai = M.ctrl[i];
-    const R qi = S.qpos[(int64_t)e * Dm + i];
-    R tgt = qi;
-    if (ai >= 0) {
-      const R a = fmin(fmax((R)act[ai], -1.0), 1.0);
-      const R lo = M.lower[i], hi = M.upper[i];
-      if (P.ctrl_mode == BS_CTRL_PD_JOINT_DELTA_POS) {
-        tgt = fmin(fmax(qi + a * P.action_scale, lo), hi);
-      } else {
-        const R un = (isfinite(lo) && isfinite(hi)) ? lo + (a + 1.0) * 0.5 * (hi - lo) : a * P.action_scale;
-        tgt = fmin(fmax(un, lo), hi);
+  if (P.ctrl_mode == BS_CTRL_PD_EE_DELTA_POSE) {
+    // DLS IK: twist = (a[0:3] * scale, a[3:6] * rot_scale), world frame, at
+    // the ee origin; dq = J^T (J J^T + lam^2 I)^-1 twist over the controlled dofs.
+    __syncwarp();
+    fk_group<G>(M, Y, E, l);
+    if (l == 0) {
+      R* Jm = E + Y.rows;        // 6 x Dm, scratch (rows are rebuilt every substep)
+      R* A = Jm + 6 * Dm;        // 6 x 6
+      for (int i = 0; i < 6 * Dm; ++i) Jm[i] = 0.0;
+      const R* lpq0 = E + Y.lpq;
+      const V3<R> pe = ld3(lpq0 + 7 * P.ee_link);
+      for (int k = P.ee_link; k >= 0; k = M.parent[k]) {
+        const int jt = M.jtype[k];
+        if (jt == BS_JOINT_FIXED) continue;
+        const int d = M.dof[k];
+        if (M.ctrl[d] < 0) continue;
+        const V3<R> a = quat_rotate(ld4(lpq0 + 7 * k + 3), ld3(M.axis + 3 * k));
+        const V3<R> lin = jt == BS_JOINT_REVOLUTE ? crs(a, sub(pe, ld3(lpq0 + 7 * k))) : a;
+        const V3<R> ang = jt == BS_JOINT_REVOLUTE ? a : v3(0, 0, 0);
+        Jm[0 * Dm + d] = lin.x; Jm[1 * Dm + d] = lin.y; Jm[2 * Dm + d] = lin.z;
+        Jm[3 * Dm + d] = ang.x; Jm[4 * Dm + d] = ang.y; Jm[5 * Dm + d] = ang.z;
+      }
+      R tw[6];
+      for (int j = 0; j < 6; ++j) {
+        const R aj = fmin(fmax((R)act[j], -1.0), 1.0);
+        tw[j] = aj * (j < 3 ? P.action_scale : P.action_scale_rot);
+      }
+      const R lam2 = P.ik_lambda * P.ik_lambda;
+      for (int i = 0; i < 6; ++i)
+        for (int j = 0; j <= i; ++j) {
+          R sacc = 0.0;
+          for (int d = 0; d < M.D; ++d) sacc += Jm[i * Dm + d] * Jm[j * Dm + d];
+          if (i == j) sacc += lam2;
+          A[i * 6 + j] = sacc;
+        }
+      for (int j = 0; j < 6; ++j) {  // Cholesky (lower), inverse diagonal kept
+        R sd = A[j * 6 + j];
+        for (int k = 0; k < j; ++k) sd -= A[j * 6 + k] * A[j * 6 + k];
+        const R inv = rsqrt(sd);
+        A[j * 6 + j] = inv;
+        for (int i = j + 1; i < 6; ++i) {
+          R t = A[i * 6 + j];
+          for (int k = 0; k < j; ++k) t -= A[i * 6 + k] * A[j * 6 + k];
+          A[i * 6 + j] = t * inv;
+        }
+      }
+      for (int i = 0; i < 6; ++i) {
+        R t = tw[i];
+        for (int k = 0; k < i; ++k) t -= A[i * 6 + k] * tw[k];
+        tw[i] = t * A[i * 6 + i];
+      }
+      for (int i = 5; i >= 0; --i) {
+        R t = tw[i];
+        for (int k = i + 1; k < 6; ++k) t -= A[k * 6 + i] * tw[k];
+        tw[i] = t * A[i * 6 + i];
+      }
+      for (int d = 0; d < M.D; ++d) {
+        const R qi = E[Y.q + d];
+        R tgt = qi;
+        if (M.ctrl[d] >= 0) {
+          R dq = 0.0;
+          for (int i = 0; i < 6; ++i) dq += Jm[i * Dm + d] * tw[i];
+          tgt = fmin(fmax(qi + dq, M.lower[d]), M.upper[d]);
+        }
+        E[Y.tgt + d] = tgt;
       }
     }
-    E[Y.tgt + i] = tgt;
+  } else {
+    for (int i = l; i < M.D; i += G) {
+      const int ai = M.ctrl[i];
+      const R qi = S.qpos[(int64_t)e * Dm + i];
+      R tgt = qi;
+      if (ai >= 0) {
+        const R a = fmin(fmax((R)act[ai], -1.0), 1.0);
+        const R lo = M.lower[i], hi = M.upper[i];
+        if (P.ctrl_mode == BS_CTRL_PD_JOINT_DELTA_POS) {
+          tgt = fmin(fmax(qi + a * P.action_scale, lo), hi);
+        } else {
+          const R un = (isfinite(lo) && isfinite(hi)) ? lo + (a + 1.0) * 0.5 * (hi - lo) : a * P.action_scale;
+          tgt = fmin(fmax(un, lo), hi);
+        }
+      }
+      E[Y.tgt + i] = tgt;
+    }
   }
   bool diverged = S.diverged[e] != 0;
   __syncwarp();

@@ -10,6 +10,8 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass, field
 
+import numpy as np
+
 from .assets import ArticulationTemplate
 
 
@@ -78,6 +80,7 @@ class ControlSpec:
     kd: float = 2.0 * math.sqrt(1000.0)
     force_limit: float = 100.0
     ik_lambda: float = 0.05
+    action_scale_rot: float = 0.05   # pd_ee_delta_pose rotation, rad per unit action (A-22)
 
 
 @dataclass(frozen=True)
@@ -118,3 +121,68 @@ def pickcube_desc(spec: PickCubeSpec) -> SceneDesc:
     arm = ArticulationDesc("arm", load_urdf(F.ARM3_URDF), tuple(spec.arm_base_p))
     cube = ActorDesc("cube", "box", (spec.cube_half,) * 3, spec.cube_density, spec.cube_color)
     return SceneDesc((arm,), (cube,), (GROUND,))
+
+
+@dataclass(frozen=True)
+class OpenCabinetSpec:
+    """Articulated-object task (BASELINE config 4; OpenChain-Hetero; A-18):
+    ARM3 on a fixed base facing a synthetic cabinet whose part count (2-6) and kinds
+    (prismatic drawer 'd' / revolute door 'r') are sampled per env at build time; one part is
+    the per-episode target; success = target joint qpos > 0.9 * upper limit."""
+
+    arm_base_p: tuple = (-0.5, 0.0, 0.25)
+    q_rest: tuple = (0.0, -0.3, 1.2)
+    q_noise: float = 0.02
+    cabinet_p: tuple = (0.1, 0.0, 0.0)
+    cabinet_yaw: float = math.pi            # front face (+x of the cabinet) towards the arm
+    min_parts: int = 2
+    max_parts: int = 6
+    success_frac: float = 0.9
+    max_steps: int = 100
+    ee_link: str = "ee"
+    control_mode: str = "pd_joint_delta_pos"
+    action_scale: float = 0.1
+    kp: float = 1000.0
+    kd: float = 2.0 * math.sqrt(1000.0)
+    force_limit: float = 100.0
+
+    def task_f(self):
+        return [self.q_noise, self.success_frac, 0.0, 0.0, 0.0, 0.0, *self.q_rest]
+
+    def control(self):
+        return ControlSpec(self.control_mode, "arm", self.action_scale, self.kp, self.kd, self.force_limit)
+
+
+TAG_SCENE = 0x5343454E  # 'SCEN': build-time per-env scene sampling stream
+
+
+def cabinet_kinds(spec: OpenCabinetSpec, num_envs: int, seed: int, env_offset: int = 0):
+    """Per-env part strings, drawn from each env's counter stream (shard-invariant)."""
+    from . import rng
+
+    ids = np.arange(env_offset, env_offset + num_envs, dtype=np.uint64)
+    u = rng.uniforms(seed, ids, 0, TAG_SCENE, 1 + spec.max_parts)
+    span = spec.max_parts - spec.min_parts + 1
+    out = []
+    for e in range(num_envs):
+        n = spec.min_parts + min(int(u[e, 0] * span), span - 1)
+        out.append("".join("d" if u[e, 1 + i] < 0.5 else "r" for i in range(n)))
+    return out
+
+
+def opencabinet_descs(spec: OpenCabinetSpec, num_envs: int, seed: int):
+    """One SceneDesc per env (heterogeneous): ARM3 + cabinet(kinds) + ground."""
+    from . import fixtures as F
+    from .assets import load_urdf
+
+    arm = ArticulationDesc("arm", load_urdf(F.ARM3_URDF), tuple(spec.arm_base_p))
+    h = 0.5 * spec.cabinet_yaw
+    cq = (math.cos(h), 0.0, 0.0, math.sin(h))
+    cache = {}
+    descs = []
+    for kinds in cabinet_kinds(spec, num_envs, seed):
+        if kinds not in cache:
+            cab = ArticulationDesc("cabinet", load_urdf(F.make_cabinet_urdf(kinds)), tuple(spec.cabinet_p), cq)
+            cache[kinds] = SceneDesc((arm, cab), (), (GROUND,))
+        descs.append(cache[kinds])
+    return descs

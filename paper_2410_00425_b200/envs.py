@@ -80,6 +80,7 @@ class Env:
         p.ctrl_mode = cabi.CTRL[ctl.mode]
         p.action_dim = self.action_dim
         p.action_scale, p.ik_lambda = ctl.action_scale, ctl.ik_lambda
+        p.action_scale_rot = getattr(ctl, "action_scale_rot", 0.05)
         p.ee_link, p.task, p.max_steps = ee_link, task, max_steps
         p.auto_reset, p.early_termination = int(auto_reset), int(early_termination)
         p.seed = self.seed & 0xFFFFFFFFFFFFFFFF

@@ -165,7 +165,7 @@ class PackedModel:
                 self.ctrl[d] = n
                 self.kp[d], self.kd[d], self.flim[d] = control.kp, control.kd, control.force_limit
                 n += 1
-        self.action_dim = n
+        self.action_dim = 6 if control.mode == "pd_ee_delta_pose" and n else n
 
 
 def _stack(models, fn, width, dtype, fill=0):

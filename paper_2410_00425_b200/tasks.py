@@ -14,7 +14,8 @@ from __future__ import annotations
 from dataclasses import replace
 
 from . import cabi
-from .descriptors import PickCubeSpec, SceneDesc, pickcube_desc  # noqa: F401
+from .descriptors import (OpenCabinetSpec, PickCubeSpec, SceneDesc, opencabinet_descs,  # noqa: F401
+                          pickcube_desc)
 from .envs import Env, SimConfig
 from .scene import build_batch
 
@@ -43,6 +44,21 @@ def _make_pickcube(num_envs, seed, overrides, obs_mode, device, shard, sim, came
     env = Env(scene, cabi.TASK_PICKCUBE, spec.task_f(), ee, spec.max_steps, seed, sim, obs_mode, renderer,
               name="PickCube", **kw)
     env.spec = spec
+    env.reset()
+    return env
+
+
+@register("OpenCabinet")
+def _make_opencabinet(num_envs, seed, overrides, obs_mode, device, shard, sim, cameras, **kw):
+    spec = replace(OpenCabinetSpec(), **(overrides or {}))
+    descs = opencabinet_descs(spec, num_envs, seed)
+    scene = build_batch(descs, seed, spec.control(), device, shard)
+    ee = scene.models[0].link_names.index(f"arm/{spec.ee_link}")
+    renderer = _renderer(scene, obs_mode, cameras, seed)
+    env = Env(scene, cabi.TASK_OPENCHAIN, spec.task_f(), ee, spec.max_steps, seed, sim, obs_mode, renderer,
+              name="OpenCabinet", **kw)
+    env.spec = spec
+    env.descs = descs
     env.reset()
     return env
 

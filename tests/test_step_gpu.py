@@ -218,3 +218,25 @@ def test_divergence_flags_and_freezes_only_that_env(cuda):
     assert bool(r.info["fail"][2]) and bool(r.terminated[2])
     assert torch.equal(env.scene.qpos[2], before["qpos"][2])  # frozen
     assert torch.isfinite(env.scene.qpos[[0, 1, 3]]).all()
+
+
+def test_ee_delta_pose_one_step_parity(cuda):
+    """pd_ee_delta_pose (DLS IK) on the device vs the oracle: targets and
+    the stepped state within 1e-9 from identical start states."""
+    from oracle.tasks import PickCubeOracle
+    from paper_2410_00425_b200.tasks import make_task, pickcube_scene
+
+    ov = {"control_mode": "pd_ee_delta_pose", "action_scale": 0.01}
+    env = make_task("PickCube", 8, seed=13, overrides=ov)
+    assert env.action_dim == 6
+    orc = PickCubeOracle(env.spec, pickcube_scene(env.spec), 8, 13)
+    rng = np.random.default_rng(0)
+    for t in range(15):
+        orc.load(gpu_snapshot(env))
+        orc.reset_count[:] = env.scene.reset_count.cpu().numpy().astype(np.uint64)
+        a = rng.uniform(-1, 1, (8, 6)).astype(np.float32)
+        env.step(torch.as_tensor(a, device=env.device))
+        orc.step(a)
+        tg = env.scene.target.cpu().numpy()[:, :3]
+        assert np.isfinite(tg).all()
+        compare(gpu_snapshot(env), orc.snapshot(), atol=1e-9, what=f"ee step {t}")
