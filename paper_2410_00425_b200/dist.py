@@ -1,0 +1,56 @@
+"""Multi-GPU plumbing: env-index sharding and the rollout-statistics collectives.
+
+Envs are independent. A batch of N global envs is therefore split into
+contiguous per-rank ranges with no data-path collective:
+- every rank builds the layout maxima from the global descriptor list;
+- every rank keys RNG streams by the global env index, so the shards compose bitwise.
+
+torch.distributed (NCCL over NVLink on the B200 box, gloo in the CPU tests) is used only
+outside the step:
+- the max-over-ranks of timings;
+- a SUM all-reduce of episode statistics (a handful of scalars per rollout,
+  SPEC.md:530-533, 588).
+"""
+
+from __future__ import annotations
+
+import torch
+
+
+def shard_range(num_envs: int, rank: int, world: int):
+    """[lo, hi) global env indices owned by `rank` (contiguous, sizes differ by at most 1)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad shard ({rank}, {world})")
+    return rank * num_envs // world, (rank + 1) * num_envs // world
+
+
+STAT_FIELDS = ("episodes", "return_sum", "length_sum", "success_once", "success_at_end", "fail_once",
+               "fail_at_end")
+
+
+def reduce_stats(stats: torch.Tensor, group=None) -> torch.Tensor:
+    """SUM all-reduce of a (len(STAT_FIELDS),) float64 statistics vector across ranks; a no-op
+    when torch.distributed is not initialised."""
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(stats, op=dist.ReduceOp.SUM, group=group)
+    return stats
+
+
+def max_over_ranks(values: torch.Tensor, group=None) -> torch.Tensor:
+    """Element-wise MAX across ranks (timings: the job is as slow as its slowest rank)."""
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(values, op=dist.ReduceOp.MAX, group=group)
+    return values
+
+
+def summarize(stats: torch.Tensor) -> dict:
+    """Mean episode metrics from a reduced statistics vector."""
+    s = dict(zip(STAT_FIELDS, (float(x) for x in stats.tolist())))
+    n = max(s["episodes"], 1.0)
+    return {"episodes": int(s["episodes"]), "mean_return": s["return_sum"] / n, "mean_length": s["length_sum"] / n,
+            "success_once": s["success_once"] / n, "success_at_end": s["success_at_end"] / n,
+            "fail_once": s["fail_once"] / n, "fail_at_end": s["fail_at_end"] / n}
