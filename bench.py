@@ -47,12 +47,16 @@ if ROOT not in sys.path:
 METRIC = "env-steps/s (sim+render, whole box)"
 FALLBACK_HBM_GBS = 6650.0
 WORKLOADS = {
-    "c2": {"envs": 4096, "obs_mode": "state",
+    "c2": {"task": "PickCube", "envs": 4096, "obs_mode": "state",
            "desc": "C2 PickCube-style (ARM3 + cube + ground), obs_mode=state, 4096 envs/GPU"},
-    "c3": {"envs": 1024, "obs_mode": "rgbd",
+    "c3": {"task": "PickCube", "envs": 1024, "obs_mode": "rgbd",
            "desc": "C3 PickCube-style, obs_mode=rgb+depth (+seg) 1 camera 128x128, 1024 envs/GPU"},
-    "c4": {"envs": 1024, "obs_mode": "pointcloud",
-           "desc": "C4-style PickCube, obs_mode=pointcloud (+seg mask) 1 camera 128x128, 1024 envs/GPU"},
+    "c4": {"task": "OpenCabinet", "envs": 1024, "obs_mode": "pointcloud",
+           "desc": "C4 OpenCabinet (ARM3 + per-env 2-6 drawer/door cabinet), obs_mode=pointcloud 1 camera "
+                   "128x128, 1024 envs/GPU"},
+    "c5": {"task": "PickHetero", "envs": 1024, "obs_mode": "rgbd",
+           "desc": "C5 PickHetero (per-env object kind/size/colour, jittered cameras), rgb+depth+seg 2 cameras "
+                   "256x256, 1024 envs/GPU"},
 }
 
 
@@ -126,7 +130,9 @@ def sim_bytes_per_env_step(scene, obs_dim, action_dim):
     Counted: the action read; articulation and actor state read and written; the drive-target
     write; goal read/write; obs and reward writes; flags and counters. Scratch (link poses,
     contact rows) is on-chip; the link-pose cache write counts as output."""
-    D, A, L = scene.models[0].D, scene.models[0].A, scene.models[0].L
+    D = max(m.D for m in scene.models)
+    A = max(m.A for m in scene.models)
+    L = max(m.L for m in scene.models)
     f8 = 8
     b = 4 * action_dim                       # action (f32)
     b += 2 * 2 * D * f8                      # qpos, qvel read + write
@@ -247,6 +253,10 @@ def run_reference(args):
     if rank != 0:
         return 0
     wl = WORKLOADS[args.config]
+    if wl["task"] != "PickCube":
+        print(json.dumps({"impl": "reference", "unavailable": f"CPU reference arm implemented for PickCube "
+                          f"workloads (c2, c3); {args.config} is {wl['task']}"}), flush=True)
+        return 0
     total = wl["envs"] * args.gpus
     rate, cores, info = cpu_reference(total, args.warmup, steps=args.steps, seed=args.seed, obs_mode=wl["obs_mode"])
     ms = total / rate * 1e3
@@ -354,7 +364,7 @@ def run_workload(name, steps, warmup, world, rank, local, dist, flush, seed, e2e
 
     wl = WORKLOADS[name]
     n_global = wl["envs"] * world
-    env = make_task("PickCube", n_global, seed=seed, obs_mode=wl["obs_mode"],
+    env = make_task(wl["task"], n_global, seed=seed, obs_mode=wl["obs_mode"],
                     shard=(rank, world) if world > 1 else None)
     N = env.num_envs
     m = measure(env, steps, warmup, flush, dist, local)
@@ -409,12 +419,12 @@ def run_ours(args):
         raise SystemExit("--gpus N>1 must be launched with torch.distributed.run (one rank per GPU)")
     # CPU baselines first (before CUDA is initialised in this process; spawn-based workers)
     cpu, cpu2 = None, None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and WORKLOADS[args.config]["task"] == "PickCube":
         wl = WORKLOADS[args.config]
         rate, cores, info = cpu_reference(wl["envs"], 2, seconds=args.cpu_seconds, seed=args.seed,
                                           obs_mode=wl["obs_mode"])
         cpu = {"value": rate, "unit": "env-steps/s", "cores": cores, "kind": "port", "sample": info}
-        if args.secondary:
+        if args.secondary and WORKLOADS[args.secondary]["task"] == "PickCube":
             w2 = WORKLOADS[args.secondary]
             n2 = 4 * len(os.sched_getaffinity(0))  # bounded sample: 4 envs per core
             rate, cores, info = cpu_reference(n2, 1, seconds=args.cpu_seconds / 2, seed=args.seed,

@@ -34,7 +34,7 @@ extern "C" {
 #define BS_ERR_UNSUPPORTED 6 /* ModelError      (errors.py:40) */
 
 /* ABI version: bumped whenever a signature or a struct layout below changes. */
-#define BS_ABI_VERSION 3
+#define BS_ABI_VERSION 4
 int bs_abi_version(void);
 
 /* Bind the library's CUDA runtime to `device` (call once per process/thread before use;
@@ -135,6 +135,7 @@ typedef struct BsModelTables {
   const int32_t* pair_slot;    /* [M][P_max] first contact slot of the pair (prefix of max contacts) */
   const double* actor_mass;    /* [M][A_max] */
   const double* actor_inertia; /* [M][A_max][3] principal, body frame            */
+  const double* actor_rest;    /* [M][A_max][5] resting height z + orientation q (reset sampling) */
 } BsModelTables;
 
 typedef struct BsEnvState {

@@ -22,18 +22,31 @@ from .model import Model
 from .philox import reset_uniforms, uniform
 
 
+def rest_pose(kind, size):
+    """DESIGN.md A-26: resting height and orientation of a free primitive on the plane --
+    upright box / sphere at half-height / radius; capsule / cylinder lying along world x."""
+    if kind in ("box",):
+        return float(size[2]), np.array([1.0, 0.0, 0.0, 0.0])
+    if kind == "sphere":
+        return float(size[0]), np.array([1.0, 0.0, 0.0, 0.0])
+    h = math.sqrt(0.5)
+    return float(size[0]), np.array([h, 0.0, h, 0.0])
+
+
 class PickCubeOracle:
     """B envs of the PickCube-style scene, stepped by the oracle engine."""
 
     N_UNIFORMS = 8
 
-    def __init__(self, spec, desc, num_envs, seed, env_offset=0, cfg=None):
+    def __init__(self, spec, desc, num_envs, seed, env_offset=0, cfg=None, env_ids=None):
         self.spec = spec
         self.model = Model(desc)
         self.cfg = cfg or E.SimConfig()
         self.B = num_envs
         self.seed = seed
-        self.env_ids = np.arange(env_offset, env_offset + num_envs, dtype=np.uint64)
+        self.env_ids = (np.arange(env_offset, env_offset + num_envs, dtype=np.uint64) if env_ids is None
+                        else np.asarray(env_ids, np.uint64))
+        self.rest_z, self.rest_q = rest_pose(desc.actors[0].kind, desc.actors[0].size)
         m = self.model
         D = m.D
         self.ee_link = m.link_names.index(f"arm/{spec.ee_link}")
@@ -64,8 +77,10 @@ class PickCubeOracle:
         gy = uniform(-s.goal_xy, s.goal_xy, u[:, 7])
         h = 0.5 * yaw
         aq = se3.qnorm(np.stack([np.cos(h), np.zeros(n), np.zeros(n), np.sin(h)], -1))
-        ap = np.stack([cx, cy, np.full(n, s.cube_half)], -1)
-        goal = np.stack([gx, gy, np.full(n, s.cube_half)], -1)
+        if tuple(self.rest_q) != (1.0, 0.0, 0.0, 0.0):
+            aq = se3.qnorm(se3.qmul(aq, np.broadcast_to(self.rest_q, aq.shape)))
+        ap = np.stack([cx, cy, np.full(n, self.rest_z)], -1)
+        goal = np.stack([gx, gy, np.full(n, self.rest_z)], -1)
         return q, ap, aq, goal
 
     def reset(self, mask=None):
@@ -239,3 +254,45 @@ class OpenCabinetOracle:
             m, idx = g["model"], g["idx"]
             g["st"].q[:] = q[idx, :m.D]
             g["st"].qd[:] = qd[idx, :m.D]
+
+
+class PickHeteroOracle:
+    """PickHetero (BASELINE config 5): envs grouped by object layout, each group a
+    PickCubeOracle over its global env ids (envs are independent)."""
+
+    def __init__(self, spec, descs, seed, cfg=None):
+        self.B = len(descs)
+        groups = {}
+        for e, d in enumerate(descs):
+            groups.setdefault(d.key(), (d, []))[1].append(e)
+        self.groups = [(np.asarray(idx), PickCubeOracle(spec, d, len(idx), seed, cfg=cfg, env_ids=idx))
+                       for d, idx in groups.values()]
+
+    def step(self, action):
+        rew = np.zeros(self.B, np.float32)
+        term = np.zeros(self.B, bool)
+        trunc = np.zeros(self.B, bool)
+        succ = np.zeros(self.B, bool)
+        for idx, o in self.groups:
+            _, r, te, tr, info, _ = o.step(np.asarray(action)[idx])
+            rew[idx], term[idx], trunc[idx], succ[idx] = r, te, tr, info["success"]
+        return rew, term, trunc, {"success": succ}
+
+    def snapshot(self):
+        out = {}
+        for idx, o in self.groups:
+            sn = o.snapshot()
+            for k, v in sn.items():
+                if k not in out:
+                    out[k] = np.zeros((self.B,) + v.shape[1:], v.dtype)
+                out[k][idx] = v
+        return out
+
+    def load(self, snap, reset_count=None):
+        for idx, o in self.groups:
+            o.load({k: v[idx] for k, v in snap.items()})
+            if reset_count is not None:
+                o.reset_count[:] = reset_count[idx]
+
+    def link_poses(self):
+        return [(idx, o.link_poses(), o) for idx, o in self.groups]

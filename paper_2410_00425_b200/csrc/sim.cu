@@ -117,7 +117,7 @@ __global__ void k_masked_copy(const uint8_t* __restrict__ src, uint8_t* __restri
 
 // capacity tiers: (MD, ML, MS, MC, MA)
 typedef Cap<4, 8, 8, 12, 2> CapSmall;     // PickCube-style (D=3, L=5, S=5, C=10, A=1)
-typedef Cap<12, 16, 24, 32, 4> CapLarge;  // cabinets / heterogeneous scenes
+typedef Cap<12, 16, 32, 64, 4> CapLarge;  // cabinets / heterogeneous scenes
 
 template <class C>
 bool fits(const BsModelTables& T) {

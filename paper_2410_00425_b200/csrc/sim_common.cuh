@@ -89,7 +89,7 @@ struct Model {
   const int32_t *s_btype, *s_body, *s_kind, *s_seg;
   const R *s_size, *s_frame, *s_radius;
   const int32_t *p_i, *p_j, *p_code, *p_slot;
-  const R *a_mass, *a_inertia;
+  const R *a_mass, *a_inertia, *a_rest;
 };
 
 __device__ __forceinline__ Model model_of(const BsModelTables& T, int m) {
@@ -106,7 +106,7 @@ __device__ __forceinline__ Model model_of(const BsModelTables& T, int m) {
   M.s_seg = T.shape_seg + so; M.s_size = T.shape_size + 3 * so; M.s_frame = T.shape_frame + 7 * so;
   M.s_radius = T.shape_radius + so;
   M.p_i = T.pair_i + po; M.p_j = T.pair_j + po; M.p_code = T.pair_code + po; M.p_slot = T.pair_slot + po;
-  M.a_mass = T.actor_mass + ao; M.a_inertia = T.actor_inertia + 3 * ao;
+  M.a_mass = T.actor_mass + ao; M.a_inertia = T.actor_inertia + 3 * ao; M.a_rest = T.actor_rest + 5 * ao;
   return M;
 }
 
@@ -207,7 +207,7 @@ __device__ __forceinline__ V3<R> m3mul(const R* A, V3<R> x) {
 // ---------------------------------------------------------------- tasks
 // PickCube task_f layout: 0 q_noise, 1 cube_half, 2 cube_xy, 3 goal_xy, 4 success_dist,
 // 5 fail_z, 6..8 q_rest.   OpenChain task_f: 0 success_frac.
-static __device__ void task_reset(const Model& M, const BsSimParams& P, int64_t genv, uint32_t rc, R* q, R* qd,
+static __device__ __noinline__ void task_reset(const Model& M, const BsSimParams& P, int64_t genv, uint32_t rc, R* q, R* qd,
                            V3<R>* ap, Q4<R>* aq, V3<R>* av, V3<R>* aw, R* goal, int32_t* target_dof) {
   uint32_t k0 = (uint32_t)(P.seed & 0xffffffffu), k1 = (uint32_t)(P.seed >> 32);
   R u[8];
@@ -225,11 +225,15 @@ static __device__ void task_reset(const Model& M, const BsSimParams& P, int64_t 
     R yaw = uni(-M_PI, M_PI, u[5]);
     R s, c;
     sincos(0.5 * yaw, &s, &c);
-    ap[0] = v3(cx, cy, f[1]);
+    // resting pose of the object (actor_rest: height, orientation; A-26)
+    const R* rest = M.a_rest;
+    ap[0] = v3(cx, cy, rest[0]);
     aq[0] = quat_normalize(Q4<R>{c, 0.0, 0.0, s});
+    if (!(rest[1] == 1.0 && rest[2] == 0.0 && rest[3] == 0.0 && rest[4] == 0.0))
+      aq[0] = quat_normalize(quat_mul(aq[0], Q4<R>{rest[1], rest[2], rest[3], rest[4]}));
     goal[0] = uni(-f[3], f[3], u[6]);
     goal[1] = uni(-f[3], f[3], u[7]);
-    goal[2] = f[1];
+    goal[2] = rest[0];
   } else if (P.task == BS_TASK_OPENCHAIN) {
     // arm dofs at q_rest (task_f 6..8), articulated-object dofs closed; target dof drawn
     for (int i = 0; i < 3 && i < M.D; ++i) q[i] = __dadd_rn(P.task_f[6 + i], uni(-P.task_f[0], P.task_f[0], u[i]));

@@ -263,9 +263,10 @@ __device__ int narrow_pair(const Model& M, int pi, const R* spq, R slop, R* cand
 // Lanes build each link's local transform (joint origin o joint motion, with the sincos),
 // then lane 0 walks the topological order composing parent o local.
 template <int G>
-__device__ __forceinline__ void fk_group(const Model& M, const Lay& Y, R* E, int l) {
+__device__ __noinline__ void fk_group(const Model& M, const Lay& Y, R* E, int l) {
   R* Tl = E + Y.Tl;
   R* lpq = E + Y.lpq;
+  #pragma unroll 1
   for (int k = l; k < M.L; k += G) {
     const R* o = M.org + 7 * k;
     V3<R> tp = ld3(o);
@@ -297,6 +298,72 @@ __device__ __forceinline__ void fk_group(const Model& M, const Lay& Y, R* E, int
   __syncwarp();
 }
 
+// pd_ee_delta_pose targets (lane 0 of the group; rarely on the hot path, kept out of line).
+__device__ __noinline__ void ee_delta_targets(const Model& M, const BsSimParams& P, const Lay& Y, R* E,
+                                              const float* act) {
+  const int Dm = Y.Dm;
+      R* Jm = E + Y.rows;        // 6 x Dm, scratch (rows are rebuilt every substep)
+  R* A = Jm + 6 * Dm;        // 6 x 6
+  for (int i = 0; i < 6 * Dm; ++i) Jm[i] = 0.0;
+  const R* lpq0 = E + Y.lpq;
+  const V3<R> pe = ld3(lpq0 + 7 * P.ee_link);
+  for (int k = P.ee_link; k >= 0; k = M.parent[k]) {
+    const int jt = M.jtype[k];
+    if (jt == BS_JOINT_FIXED) continue;
+    const int d = M.dof[k];
+    if (M.ctrl[d] < 0) continue;
+    const V3<R> a = quat_rotate(ld4(lpq0 + 7 * k + 3), ld3(M.axis + 3 * k));
+    const V3<R> lin = jt == BS_JOINT_REVOLUTE ? crs(a, sub(pe, ld3(lpq0 + 7 * k))) : a;
+    const V3<R> ang = jt == BS_JOINT_REVOLUTE ? a : v3(0, 0, 0);
+    Jm[0 * Dm + d] = lin.x; Jm[1 * Dm + d] = lin.y; Jm[2 * Dm + d] = lin.z;
+    Jm[3 * Dm + d] = ang.x; Jm[4 * Dm + d] = ang.y; Jm[5 * Dm + d] = ang.z;
+  }
+  R tw[6];
+  for (int j = 0; j < 6; ++j) {
+    const R aj = fmin(fmax((R)act[j], -1.0), 1.0);
+    tw[j] = aj * (j < 3 ? P.action_scale : P.action_scale_rot);
+  }
+  const R lam2 = P.ik_lambda * P.ik_lambda;
+  for (int i = 0; i < 6; ++i)
+    for (int j = 0; j <= i; ++j) {
+      R sacc = 0.0;
+      for (int d = 0; d < M.D; ++d) sacc += Jm[i * Dm + d] * Jm[j * Dm + d];
+      if (i == j) sacc += lam2;
+      A[i * 6 + j] = sacc;
+    }
+  for (int j = 0; j < 6; ++j) {  // Cholesky (lower), inverse diagonal kept
+    R sd = A[j * 6 + j];
+    for (int k = 0; k < j; ++k) sd -= A[j * 6 + k] * A[j * 6 + k];
+    const R inv = rsqrt(sd);
+    A[j * 6 + j] = inv;
+    for (int i = j + 1; i < 6; ++i) {
+      R t = A[i * 6 + j];
+      for (int k = 0; k < j; ++k) t -= A[i * 6 + k] * A[j * 6 + k];
+      A[i * 6 + j] = t * inv;
+    }
+  }
+  for (int i = 0; i < 6; ++i) {
+    R t = tw[i];
+    for (int k = 0; k < i; ++k) t -= A[i * 6 + k] * tw[k];
+    tw[i] = t * A[i * 6 + i];
+  }
+  for (int i = 5; i >= 0; --i) {
+    R t = tw[i];
+    for (int k = i + 1; k < 6; ++k) t -= A[k * 6 + i] * tw[k];
+    tw[i] = t * A[i * 6 + i];
+  }
+  for (int d = 0; d < M.D; ++d) {
+    const R qi = E[Y.q + d];
+    R tgt = qi;
+    if (M.ctrl[d] >= 0) {
+      R dq = 0.0;
+      for (int i = 0; i < 6; ++i) dq += Jm[i * Dm + d] * tw[i];
+      tgt = fmin(fmax(qi + dq, M.lower[d]), M.upper[d]);
+    }
+    E[Y.tgt + d] = tgt;
+  }
+    }
+
 // ------------------------------------------------------------------ one substep
 template <class K>
 __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E, const int l, const int g,
@@ -320,9 +387,13 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
   // ---- A: per-link motion subspace + world inertia, per-shape world pose, per-actor free
   //         motion (gyroscopic + gravity), zero the mass matrix
   const V3<R> grav = v3(P.gravity[0], P.gravity[1], P.gravity[2]);
+  #pragma unroll 1
   for (int i = l; i < D * Dm; i += G) Mt[i] = 0.0;
+  #pragma unroll 1
   for (int i = D + l; i < Dm; i += G) E[Y.u + i] = 0.0;
+  #pragma unroll 1
   for (int i = Dm + 6 * A + l; i < Y.NU; i += G) E[Y.u + i] = 0.0;
+  #pragma unroll 1
   for (int t = l; t < L + NS + A; t += G) {
     if (t < L) {
       const int k = t, jt = M.jtype[k];
@@ -381,6 +452,7 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
   }
   __syncwarp();
   // ---- C: link forces F = I a + V x* I V (parallel over links)
+  #pragma unroll 1
   for (int k = l; k < L; k += G) {
     const Inertia I = ldI(In + 10 * k);
     const V6 Vk = ld6(V + 6 * k);
@@ -404,6 +476,7 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
   }
   __syncwarp();
   // ---- E: CRBA mass matrix (parallel over dof links)
+  #pragma unroll 1
   for (int k = l; k < L; k += G) {
     if (M.jtype[k] == BS_JOINT_FIXED) continue;
     const int i = M.dof[k];
@@ -441,6 +514,7 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
   }
   __syncwarp();
   // ---- G: columns of M^-1 (lanes j < D) and the unconstrained velocity (lane D)
+  #pragma unroll 1
   for (int j = l; j <= D; j += G) {
     R x[MD];
 #pragma unroll
@@ -477,9 +551,11 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
   // ---- H: broadphase + narrowphase into fixed per-pair candidate slots (A-5)
   R* cand = E + Y.rows;  // candidates alias the (not yet built) row storage
   const R slop = P.slop;
+  #pragma unroll 1
   for (int s = l; s < Y.Cm; s += G) cand[8 * s + 7] = -1.0;
   __syncwarp();
   int unsup = 0;
+  #pragma unroll 1
   for (int pi = l; pi < M.P; pi += G) {
     unsup += narrow_pair(M, pi, spq, slop, cand + 8 * M.p_slot[pi]);
   }
@@ -509,6 +585,7 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
   // ---- J: constraint rows (normal, t1, t2 per contact; parallel over rows)
   R* rows = E + Y.rows;
   const int RW = Y.RW, NU = Y.NU;
+  #pragma unroll 1
   for (int r = l; r < 3 * nc; r += G) {
     const int c = r / 3, rr = r - 3 * c;
     const R* cc = ct + 8 * c;
@@ -705,11 +782,14 @@ __global__ void __launch_bounds__(32) k_step(BsModelTables T, BsEnvState S, BsSt
   const int Dm = Y.Dm, Am = Y.Am;
 
   // ---- stage the env's state rows
+  #pragma unroll 1
   for (int i = l; i < Dm; i += G) {
     E[Y.q + i] = S.qpos[(int64_t)e * Dm + i];
     E[Y.qd + i] = S.qvel[(int64_t)e * Dm + i];
   }
+  #pragma unroll 1
   for (int i = l; i < 7 * Am; i += G) E[Y.apose + i] = S.actor_pose[(int64_t)e * 7 * Am + i];
+  #pragma unroll 1
   for (int i = l; i < 6 * Am; i += G) E[Y.avel + i] = S.actor_vel[(int64_t)e * 6 * Am + i];
   if (l < 3) E[Y.goal + l] = S.goal[3 * (int64_t)e + l];
   // ---- controller: drive targets, once per control step
@@ -719,69 +799,9 @@ __global__ void __launch_bounds__(32) k_step(BsModelTables T, BsEnvState S, BsSt
     // the ee origin; dq = J^T (J J^T + lam^2 I)^-1 twist over the controlled dofs.
     __syncwarp();
     fk_group<G>(M, Y, E, l);
-    if (l == 0) {
-      R* Jm = E + Y.rows;        // 6 x Dm, scratch (rows are rebuilt every substep)
-      R* A = Jm + 6 * Dm;        // 6 x 6
-      for (int i = 0; i < 6 * Dm; ++i) Jm[i] = 0.0;
-      const R* lpq0 = E + Y.lpq;
-      const V3<R> pe = ld3(lpq0 + 7 * P.ee_link);
-      for (int k = P.ee_link; k >= 0; k = M.parent[k]) {
-        const int jt = M.jtype[k];
-        if (jt == BS_JOINT_FIXED) continue;
-        const int d = M.dof[k];
-        if (M.ctrl[d] < 0) continue;
-        const V3<R> a = quat_rotate(ld4(lpq0 + 7 * k + 3), ld3(M.axis + 3 * k));
-        const V3<R> lin = jt == BS_JOINT_REVOLUTE ? crs(a, sub(pe, ld3(lpq0 + 7 * k))) : a;
-        const V3<R> ang = jt == BS_JOINT_REVOLUTE ? a : v3(0, 0, 0);
-        Jm[0 * Dm + d] = lin.x; Jm[1 * Dm + d] = lin.y; Jm[2 * Dm + d] = lin.z;
-        Jm[3 * Dm + d] = ang.x; Jm[4 * Dm + d] = ang.y; Jm[5 * Dm + d] = ang.z;
-      }
-      R tw[6];
-      for (int j = 0; j < 6; ++j) {
-        const R aj = fmin(fmax((R)act[j], -1.0), 1.0);
-        tw[j] = aj * (j < 3 ? P.action_scale : P.action_scale_rot);
-      }
-      const R lam2 = P.ik_lambda * P.ik_lambda;
-      for (int i = 0; i < 6; ++i)
-        for (int j = 0; j <= i; ++j) {
-          R sacc = 0.0;
-          for (int d = 0; d < M.D; ++d) sacc += Jm[i * Dm + d] * Jm[j * Dm + d];
-          if (i == j) sacc += lam2;
-          A[i * 6 + j] = sacc;
-        }
-      for (int j = 0; j < 6; ++j) {  // Cholesky (lower), inverse diagonal kept
-        R sd = A[j * 6 + j];
-        for (int k = 0; k < j; ++k) sd -= A[j * 6 + k] * A[j * 6 + k];
-        const R inv = rsqrt(sd);
-        A[j * 6 + j] = inv;
-        for (int i = j + 1; i < 6; ++i) {
-          R t = A[i * 6 + j];
-          for (int k = 0; k < j; ++k) t -= A[i * 6 + k] * A[j * 6 + k];
-          A[i * 6 + j] = t * inv;
-        }
-      }
-      for (int i = 0; i < 6; ++i) {
-        R t = tw[i];
-        for (int k = 0; k < i; ++k) t -= A[i * 6 + k] * tw[k];
-        tw[i] = t * A[i * 6 + i];
-      }
-      for (int i = 5; i >= 0; --i) {
-        R t = tw[i];
-        for (int k = i + 1; k < 6; ++k) t -= A[k * 6 + i] * tw[k];
-        tw[i] = t * A[i * 6 + i];
-      }
-      for (int d = 0; d < M.D; ++d) {
-        const R qi = E[Y.q + d];
-        R tgt = qi;
-        if (M.ctrl[d] >= 0) {
-          R dq = 0.0;
-          for (int i = 0; i < 6; ++i) dq += Jm[i * Dm + d] * tw[i];
-          tgt = fmin(fmax(qi + dq, M.lower[d]), M.upper[d]);
-        }
-        E[Y.tgt + d] = tgt;
-      }
-    }
+    if (l == 0) ee_delta_targets(M, P, Y, E, act);
   } else {
+    #pragma unroll 1
     for (int i = l; i < M.D; i += G) {
       const int ai = M.ctrl[i];
       const R qi = S.qpos[(int64_t)e * Dm + i];
@@ -807,6 +827,7 @@ __global__ void __launch_bounds__(32) k_step(BsModelTables T, BsEnvState S, BsSt
     substep<K>(M, P, Y, E, l, g, diverged, unsupported, nc);
     if (s == P.substeps - 1 && O.contact_count && live) {  // ContactSet of the last substep
       const R* ct = E + Y.ct;
+      #pragma unroll 1
       for (int c = l; c < nc && c < T.C_max; c += G) {
         const int64_t o = (int64_t)e * T.C_max + c;
         const int pi = (int)ct[8 * c + 7];
@@ -878,14 +899,18 @@ __global__ void __launch_bounds__(32) k_step(BsModelTables T, BsEnvState S, BsSt
   }
   if (!live) return;
   // ---- write back the state rows, the FK cache and the state observation
+  #pragma unroll 1
   for (int i = l; i < Dm; i += G) {
     S.qpos[(int64_t)e * Dm + i] = E[Y.q + i];
     S.qvel[(int64_t)e * Dm + i] = E[Y.qd + i];
     if (i < M.D) S.target[(int64_t)e * Dm + i] = E[Y.tgt + i];
   }
+  #pragma unroll 1
   for (int i = l; i < 7 * M.A; i += G) S.actor_pose[(int64_t)e * 7 * Am + i] = E[Y.apose + i];
+  #pragma unroll 1
   for (int i = l; i < 6 * M.A; i += G) S.actor_vel[(int64_t)e * 6 * Am + i] = E[Y.avel + i];
   if (l < 3) S.goal[3 * (int64_t)e + l] = E[Y.goal + l];
+  #pragma unroll 1
   for (int i = l; i < 7 * M.L; i += G) S.link_pose[(int64_t)e * 7 * Y.Lm + i] = lpq[i];
   if (l == 0) {
     S.elapsed[e] = el;
@@ -896,6 +921,7 @@ __global__ void __launch_bounds__(32) k_step(BsModelTables T, BsEnvState S, BsSt
     //   per actor slot: p[3] q[4] v[3] w[3]   goal[3]   zero padding
     float* o = O.obs + (int64_t)e * O.obs_dim;
     const int b_ee = 2 * Dm, b_act = b_ee + 3, b_goal = b_act + 13 * Am;
+    #pragma unroll 1
     for (int k = l; k < O.obs_dim; k += G) {
       R v = 0.0;
       if (k < Dm) v = k < M.D ? E[Y.q + k] : 0.0;

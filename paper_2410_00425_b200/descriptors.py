@@ -56,6 +56,20 @@ class StaticDesc:
                 tuple(self.color))
 
 
+def actor_rest_pose(kind: str, size) -> tuple:
+    """Resting height and orientation of a free primitive on the ground plane (DESIGN.md
+    A-26): boxes and spheres upright at their half-height / radius; capsules and cylinders
+    lie on their side (local z axis rotated onto world x)."""
+    if kind == "box":
+        return (float(size[2]), 1.0, 0.0, 0.0, 0.0)
+    if kind == "sphere":
+        return (float(size[0]), 1.0, 0.0, 0.0, 0.0)
+    if kind in ("capsule", "cylinder"):
+        h = math.sqrt(0.5)
+        return (float(size[0]), h, 0.0, h, 0.0)
+    raise ValueError(f"no resting pose for actor kind {kind!r}")
+
+
 @dataclass(frozen=True)
 class SceneDesc:
     articulations: tuple = ()
@@ -185,4 +199,55 @@ def opencabinet_descs(spec: OpenCabinetSpec, num_envs: int, seed: int):
             cab = ArticulationDesc("cabinet", load_urdf(F.make_cabinet_urdf(kinds)), tuple(spec.cabinet_p), cq)
             cache[kinds] = SceneDesc((arm, cab), (), (GROUND,))
         descs.append(cache[kinds])
+    return descs
+
+
+@dataclass(frozen=True)
+class PickHeteroSpec(PickCubeSpec):
+    """Heterogeneous tabletop (BASELINE config 5): every env gets its own object
+    kind (sphere / box / capsule -- the SPEC.md:339 pair set), size level in
+    [size_lo, size_hi] and colour (texture randomisation), and its own jittered
+    cameras (+-2 cm, +-2 deg)."""
+
+    kinds: tuple = ("sphere", "box", "capsule")
+    size_lo: float = 0.015
+    size_hi: float = 0.035
+    size_levels: int = 9
+    camera_res: int = 256
+    camera_pos_jitter: float = 0.02
+    camera_rot_jitter: float = math.radians(2.0)
+
+
+def hetero_objects(spec: PickHeteroSpec, num_envs: int, seed: int, env_offset: int = 0):
+    """Per-env (kind, size tuple, rgb) from each env's build-time counter stream."""
+    from . import rng
+
+    ids = np.arange(env_offset, env_offset + num_envs, dtype=np.uint64)
+    u = rng.uniforms(seed, ids, 1, TAG_SCENE, 5)
+    out = []
+    nk, nl = len(spec.kinds), spec.size_levels
+    for e in range(num_envs):
+        kind = spec.kinds[min(int(u[e, 0] * nk), nk - 1)]
+        lev = min(int(u[e, 1] * nl), nl - 1)
+        sz = spec.size_lo + lev * (spec.size_hi - spec.size_lo) / max(nl - 1, 1)
+        size = {"sphere": (sz,), "box": (sz, sz, sz), "capsule": (sz, sz)}[kind]
+        out.append((kind, size, (float(u[e, 2]), float(u[e, 3]), float(u[e, 4]))))
+    return out
+
+
+def hetero_descs(spec: PickHeteroSpec, num_envs: int, seed: int):
+    """One SceneDesc per env: ARM3 + that env's object + ground (colours are per-env render
+    inputs, not part of the layout, so envs with the same kind/size share a model)."""
+    from . import fixtures as F
+    from .assets import load_urdf
+
+    arm = ArticulationDesc("arm", load_urdf(F.ARM3_URDF), tuple(spec.arm_base_p))
+    cache = {}
+    descs = []
+    for kind, size, _ in hetero_objects(spec, num_envs, seed):
+        key = (kind, size)
+        if key not in cache:
+            obj = ActorDesc("object", kind, size, spec.cube_density, (0.5, 0.5, 0.5, 1.0))
+            cache[key] = SceneDesc((arm,), (obj,), (GROUND,))
+        descs.append(cache[key])
     return descs

@@ -19,7 +19,9 @@ import math
 import numpy as np
 
 SEGMENTS = 16          # around capsule / cylinder axes
-CAPSULE_RINGS = 8      # latitude rings per hemisphere (equator included)
+CAPSULE_RINGS = 6      # latitude rings per hemisphere (equator included)
+CAPSULE_BANDS = 5      # segments along the capsule's cylindrical side (short triangles, small
+                       # bounding boxes): 2 * (16 + 32 * 5) + 32 * 5 = 512 triangles
 GROUND_EXTENT = 1.0    # ground grid half-extent, m
 GROUND_CELLS = 8       # ground grid cells per side
 
@@ -70,13 +72,18 @@ def _capsule(r: float, hl: float):
         for s in range(S):
             ph = 2 * math.pi * s / S
             verts.append((r * math.sin(th) * math.cos(ph), r * math.sin(th) * math.sin(ph), hl + r * math.cos(th)))
+    for b in range(1, CAPSULE_BANDS):  # intermediate rings along the side
+        z = hl - 2.0 * hl * b / CAPSULE_BANDS
+        for s in range(S):
+            ph = 2 * math.pi * s / S
+            verts.append((r * math.cos(ph), r * math.sin(ph), z))
     for k in range(K, 0, -1):     # bottom hemisphere rings, equator first
         th = (math.pi / 2) * k / K
         for s in range(S):
             ph = 2 * math.pi * s / S
             verts.append((r * math.sin(th) * math.cos(ph), r * math.sin(th) * math.sin(ph), -hl - r * math.cos(th)))
     verts.append((0.0, 0.0, -hl - r))  # bottom pole
-    nring = 2 * K
+    nring = 2 * K + CAPSULE_BANDS - 1
     ring = lambda k, s: 1 + k * S + (s % S)  # noqa: E731
     f = []
     for s in range(S):

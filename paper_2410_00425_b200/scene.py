@@ -30,7 +30,7 @@ import torch
 from . import _native as nat
 from . import cabi
 from . import hostmath as hm
-from .descriptors import ControlSpec, SceneDesc  # noqa: F401
+from .descriptors import ControlSpec, SceneDesc, actor_rest_pose  # noqa: F401
 from .errors import DimensionError, LayoutMismatchError, SceneBuildError, ViewLookupError
 
 
@@ -236,12 +236,14 @@ class SceneBatch:
             ("shape_body", (M, Sm), i32), ("shape_kind", (M, Sm), i32), ("shape_seg", (M, Sm), i32),
             ("shape_size", (M, Sm, 3), f64), ("shape_frame", (M, Sm, 7), f64), ("shape_radius", (M, Sm), f64),
             ("shape_color", (M, Sm, 4), np.float32), ("pair_i", (M, Pm), i32), ("pair_j", (M, Pm), i32),
-            ("pair_code", (M, Pm), i32), ("pair_slot", (M, Pm), i32), ("actor_mass", (M, Am), f64), ("actor_inertia", (M, Am, 3), f64)]}
+            ("pair_code", (M, Pm), i32), ("pair_slot", (M, Pm), i32), ("actor_mass", (M, Am), f64), ("actor_inertia", (M, Am, 3), f64),
+            ("actor_rest", (M, Am, 5), f64)]}
         t["link_parent"][:] = -2
         t["link_dof"][:] = -1
         t["dof_ctrl"][:] = -1
         t["link_org"][..., 3] = 1.0
         t["shape_frame"][..., 3] = 1.0
+        t["actor_rest"][..., 1] = 1.0
         for m, pm in enumerate(self.models):
             t["n_links"][m], t["n_dof"][m], t["n_shapes"][m] = pm.L, pm.D, pm.S
             t["n_pairs"][m], t["n_actors"][m] = pm.P, pm.A
@@ -278,6 +280,8 @@ class SceneBatch:
             for a, (mass, inertia) in enumerate(pm.actors):
                 t["actor_mass"][m, a] = mass
                 t["actor_inertia"][m, a] = inertia
+                ad = pm.desc.actors[a]
+                t["actor_rest"][m, a] = actor_rest_pose(ad.kind, ad.size)
         self.host_tables = t
         self.tables = {k: self._t(v, torch.int32 if v.dtype == np.int32 else
                                   torch.float32 if v.dtype == np.float32 else torch.float64)

@@ -14,8 +14,8 @@ from __future__ import annotations
 from dataclasses import replace
 
 from . import cabi
-from .descriptors import (OpenCabinetSpec, PickCubeSpec, SceneDesc, opencabinet_descs,  # noqa: F401
-                          pickcube_desc)
+from .descriptors import (OpenCabinetSpec, PickCubeSpec, PickHeteroSpec, SceneDesc, hetero_descs,  # noqa: F401
+                          hetero_objects, opencabinet_descs, pickcube_desc)
 from .envs import Env, SimConfig
 from .scene import build_batch
 
@@ -63,12 +63,48 @@ def _make_opencabinet(num_envs, seed, overrides, obs_mode, device, shard, sim, c
     return env
 
 
-def _renderer(scene, obs_mode, cameras, seed):
+@register("PickHetero")
+def _make_pickhetero(num_envs, seed, overrides, obs_mode, device, shard, sim, cameras, **kw):
+    import numpy as np
+
+    from .cameras import CameraConfig, CameraJitter, look_at, pinhole
+
+    spec = replace(PickHeteroSpec(), **(overrides or {}))
+    descs = hetero_descs(spec, num_envs, seed)
+    scene = build_batch(descs, seed, spec.control(), device, shard)
+    ee = scene.models[0].link_names.index(f"arm/{spec.ee_link}")
+    renderer = None
+    if obs_mode != "state":
+        res = spec.camera_res
+        if cameras is None:
+            views = [("base_camera", (0.15, 0.5, 0.4)), ("side_camera", (0.15, -0.5, 0.4))]
+            cameras = [CameraConfig(n, pose_p=eye, pose_q=look_at(eye, (-0.15, 0.0, 0.02)), **pinhole(res, res, 60.0))
+                       for n, eye in views]
+        objs = hetero_objects(spec, num_envs, seed)[scene.env_offset:scene.env_offset + scene.num_envs]
+        colors = scene.host_tables["shape_color"][scene.model_index, :, :3].astype(np.float32).copy()
+        for e, (_, _, rgb) in enumerate(objs):
+            pm = scene.models[scene.model_index[e]]
+            for s_idx, sh in enumerate(pm.shapes):
+                if sh["btype"] == cabi.BODY_ACTOR:
+                    colors[e, s_idx] = rgb
+        renderer = _renderer(scene, obs_mode, cameras, seed,
+                             CameraJitter(spec.camera_pos_jitter, spec.camera_rot_jitter, 0.0), colors)
+    env = Env(scene, cabi.TASK_PICKCUBE, spec.task_f(), ee, spec.max_steps, seed, sim, obs_mode, renderer,
+              name="PickHetero", **kw)
+    env.spec = spec
+    env.descs = descs
+    env.reset()
+    return env
+
+
+def _renderer(scene, obs_mode, cameras, seed, jitter=None, env_color=None):
     if obs_mode == "state":
         return None
+    from .cameras import CameraJitter
     from .render import Renderer, default_cameras
 
-    return Renderer(scene, cameras if cameras is not None else default_cameras(), obs_mode, seed)
+    return Renderer(scene, cameras if cameras is not None else default_cameras(), obs_mode, seed,
+                    jitter or CameraJitter(), env_color=env_color)
 
 
 def make_task(name: str, num_envs: int, seed: int = 0, overrides=None, obs_mode: str = "state", device=None,
