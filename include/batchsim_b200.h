@@ -34,7 +34,7 @@ extern "C" {
 #define BS_ERR_UNSUPPORTED 6 /* ModelError      (errors.py:40) */
 
 /* ABI version: bumped whenever a signature or a struct layout below changes. */
-#define BS_ABI_VERSION 4
+#define BS_ABI_VERSION 5
 int bs_abi_version(void);
 
 /* Bind the library's CUDA runtime to `device` (call once per process/thread before use;
@@ -153,6 +153,8 @@ typedef struct BsEnvState {
   int32_t* elapsed;            /* [N] steps in the current episode               */
   uint32_t* reset_count;       /* [N] episodes started (RNG counter)             */
   int32_t* target_dof;         /* [N] task-designated dof (OpenChain) or -1      */
+  double* ep_return;           /* [N] running episode return (EpisodeMetrics) */
+  uint8_t* ep_flags;           /* [N] bit0 success_once, bit1 fail_once (running) */
 } BsEnvState;
 
 typedef struct BsStepOutputs {
@@ -167,6 +169,11 @@ typedef struct BsStepOutputs {
   int32_t* contact_count;      /* [N] contacts in the last substep (may be NULL) */
   int32_t* contact_pairs;      /* [N][C_max][2] shape slots (may be NULL)        */
   double* contact_geom;        /* [N][C_max][7] point, normal, depth (may be NULL) */
+  /* EpisodeMetrics of episodes that ended this step; may all be NULL */
+  uint8_t* ep_done;            /* [N] 1 = an episode ended (terminated or truncated) */
+  double* ep_return_out;       /* [N] its return (sum of the step rewards)         */
+  int32_t* ep_length_out;      /* [N] its length in steps                          */
+  uint8_t* ep_flags_out;       /* [N] bit0 success_once bit1 success_at_end bit2 fail_once bit3 fail_at_end */
 } BsStepOutputs;
 
 typedef struct BsSimParams {

@@ -25,13 +25,14 @@ class BsModelTables(ctypes.Structure):
 class BsEnvState(ctypes.Structure):
     _fields_ = [("num_envs", I32), ("env_offset", I64)] + [
         (n, P) for n in ("model_id", "qpos", "qvel", "target", "actor_pose", "actor_vel", "link_pose", "goal",
-                         "diverged", "elapsed", "reset_count", "target_dof")]
+                         "diverged", "elapsed", "reset_count", "target_dof", "ep_return", "ep_flags")]
 
 
 class BsStepOutputs(ctypes.Structure):
     _fields_ = [("obs", P), ("obs_dim", I32)] + [
         (n, P) for n in ("reward", "terminated", "truncated", "success", "fail", "unsupported_pairs",
-                         "contact_count", "contact_pairs", "contact_geom")]
+                         "contact_count", "contact_pairs", "contact_geom", "ep_done", "ep_return_out",
+                         "ep_length_out", "ep_flags_out")]
 
 
 class BsSimParams(ctypes.Structure):

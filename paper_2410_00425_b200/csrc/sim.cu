@@ -66,6 +66,8 @@ __global__ void __launch_bounds__(64) k_reset(BsModelTables T, BsEnvState S, BsS
     S.target_dof[e] = tdof;
     S.elapsed[e] = 0;
     S.diverged[e] = 0;
+    if (S.ep_return) S.ep_return[e] = 0.0;
+    if (S.ep_flags) S.ep_flags[e] = 0;
     for (int i = 0; i < M.D; ++i) r.tgt[i] = r.q[i];
   } else {
     const R* tg = S.target + (int64_t)e * T.D_max;

@@ -207,6 +207,31 @@ __device__ __forceinline__ V3<R> m3mul(const R* A, V3<R> x) {
 // ---------------------------------------------------------------- tasks
 // PickCube task_f layout: 0 q_noise, 1 cube_half, 2 cube_xy, 3 goal_xy, 4 success_dist,
 // 5 fail_z, 6..8 q_rest.   OpenChain task_f: 0 success_frac.
+
+// Reference-order quaternion product / normalisation with every operation rounded separately
+// (no FMA contraction even in FMA-enabled translation units): reset sampling must equal the
+// numpy oracle bit for bit (pose.py:31-55 order).
+__device__ __forceinline__ Q4<R> qmul_rn(const Q4<R>& a, const Q4<R>& b) {
+  Q4<R> o;
+  o.w = __dsub_rn(__dsub_rn(__dsub_rn(__dmul_rn(a.w, b.w), __dmul_rn(a.x, b.x)), __dmul_rn(a.y, b.y)), __dmul_rn(a.z, b.z));
+  o.x = __dsub_rn(__dadd_rn(__dadd_rn(__dmul_rn(a.w, b.x), __dmul_rn(a.x, b.w)), __dmul_rn(a.y, b.z)), __dmul_rn(a.z, b.y));
+  o.y = __dadd_rn(__dadd_rn(__dsub_rn(__dmul_rn(a.w, b.y), __dmul_rn(a.x, b.z)), __dmul_rn(a.y, b.w)), __dmul_rn(a.z, b.x));
+  o.z = __dadd_rn(__dsub_rn(__dadd_rn(__dmul_rn(a.w, b.z), __dmul_rn(a.x, b.y)), __dmul_rn(a.y, b.x)), __dmul_rn(a.z, b.w));
+  return o;
+}
+__device__ __forceinline__ Q4<R> qnorm_rn(Q4<R> q) {
+  R ss = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(q.w, q.w), __dmul_rn(q.x, q.x)), __dmul_rn(q.y, q.y)), __dmul_rn(q.z, q.z));
+  R n = __dsqrt_rn(ss);
+  Q4<R> r{__ddiv_rn(q.w, n), __ddiv_rn(q.x, n), __ddiv_rn(q.y, n), __ddiv_rn(q.z, n)};
+  R s = 0.0;
+  if (s == 0.0) s = sign_like_numpy(r.w);
+  if (s == 0.0) s = sign_like_numpy(r.x);
+  if (s == 0.0) s = sign_like_numpy(r.y);
+  if (s == 0.0) s = sign_like_numpy(r.z);
+  if (s == 0.0) s = 1.0;
+  return Q4<R>{__dmul_rn(r.w, s), __dmul_rn(r.x, s), __dmul_rn(r.y, s), __dmul_rn(r.z, s)};
+}
+
 static __device__ __noinline__ void task_reset(const Model& M, const BsSimParams& P, int64_t genv, uint32_t rc, R* q, R* qd,
                            V3<R>* ap, Q4<R>* aq, V3<R>* av, V3<R>* aw, R* goal, int32_t* target_dof) {
   uint32_t k0 = (uint32_t)(P.seed & 0xffffffffu), k1 = (uint32_t)(P.seed >> 32);
@@ -228,9 +253,9 @@ static __device__ __noinline__ void task_reset(const Model& M, const BsSimParams
     // resting pose of the object (actor_rest: height, orientation; A-26)
     const R* rest = M.a_rest;
     ap[0] = v3(cx, cy, rest[0]);
-    aq[0] = quat_normalize(Q4<R>{c, 0.0, 0.0, s});
+    aq[0] = qnorm_rn(Q4<R>{c, 0.0, 0.0, s});
     if (!(rest[1] == 1.0 && rest[2] == 0.0 && rest[3] == 0.0 && rest[4] == 0.0))
-      aq[0] = quat_normalize(quat_mul(aq[0], Q4<R>{rest[1], rest[2], rest[3], rest[4]}));
+      aq[0] = qnorm_rn(qmul_rn(aq[0], Q4<R>{rest[1], rest[2], rest[3], rest[4]}));
     goal[0] = uni(-f[3], f[3], u[6]);
     goal[1] = uni(-f[3], f[3], u[7]);
     goal[2] = rest[0];

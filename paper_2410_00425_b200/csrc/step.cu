@@ -872,6 +872,23 @@ __global__ void __launch_bounds__(32) k_step(BsModelTables T, BsEnvState S, BsSt
     O.success[e] = success;
     O.fail[e] = fail;
     O.unsupported_pairs[e] = unsupported;
+    // EpisodeMetrics: return = sum of rewards, *_once latch, *_at_end
+    // sampled at the final step; emitted when the episode ends, accumulators restart.
+    if (S.ep_return) {
+      const double ret = S.ep_return[e] + (double)reward;
+      const uint8_t fl = S.ep_flags[e] | (success ? 1 : 0) | (fail ? 2 : 0);
+      const bool ended = terminated || truncated;
+      if (O.ep_done) {
+        O.ep_done[e] = ended;
+        if (ended) {
+          O.ep_return_out[e] = ret;
+          O.ep_length_out[e] = el;
+          O.ep_flags_out[e] = (fl & 1) | (success ? 2 : 0) | ((fl & 2) << 1) | (fail ? 8 : 0);
+        }
+      }
+      S.ep_return[e] = ended ? 0.0 : ret;
+      S.ep_flags[e] = ended ? 0 : fl;
+    }
   }
   // ---- in-kernel auto-reset from the env's Philox stream
   const bool done = live && P.auto_reset && (terminated || truncated);

@@ -100,12 +100,18 @@ class Env:
         self.contact_pairs = torch.zeros((N, scene.C_max, 2), dtype=torch.int32, device=dev)
         self.contact_geom = torch.zeros((N, scene.C_max, 7), dtype=torch.float64, device=dev)
         self.action_buf = torch.zeros((N, max(1, self.action_dim)), dtype=torch.float32, device=dev)
+        self.ep_done = torch.zeros(N, dtype=torch.uint8, device=dev)
+        self.ep_return_out = torch.zeros(N, dtype=torch.float64, device=dev)
+        self.ep_length_out = torch.zeros(N, dtype=torch.int32, device=dev)
+        self.ep_flags_out = torch.zeros(N, dtype=torch.uint8, device=dev)
         o = cabi.BsStepOutputs()
         o.obs, o.obs_dim = self.state_obs.data_ptr(), self.obs_dim
         for k, t in (("reward", self.reward), ("terminated", self.terminated), ("truncated", self.truncated),
                      ("success", self.success), ("fail", self.fail), ("unsupported_pairs", self.unsupported),
                      ("contact_count", self.contact_count), ("contact_pairs", self.contact_pairs),
-                     ("contact_geom", self.contact_geom)):
+                     ("contact_geom", self.contact_geom), ("ep_done", self.ep_done),
+                     ("ep_return_out", self.ep_return_out), ("ep_length_out", self.ep_length_out),
+                     ("ep_flags_out", self.ep_flags_out)):
             setattr(o, k, t.data_ptr())
         self.c_out = o
         self._graph = None
@@ -227,7 +233,9 @@ class Env:
     def _result(self) -> StepResult:
         info = {"success": self.success, "fail": self.fail, "unsupported_pairs": self.unsupported,
                 "elapsed": self.scene.elapsed, "diverged": self.scene.diverged,
-                "contact_count": self.contact_count}
+                "contact_count": self.contact_count,
+                "episode": {"done": self.ep_done, "return": self.ep_return_out, "length": self.ep_length_out,
+                            "flags": self.ep_flags_out}}
         return StepResult(self._obs(), self.reward, self.terminated, self.truncated, info)
 
     def contacts(self):

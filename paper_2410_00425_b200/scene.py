@@ -311,6 +311,8 @@ class SceneBatch:
         self.elapsed = torch.zeros(N, dtype=torch.int32, device=dev)
         self.reset_count = torch.zeros(N, dtype=torch.int32, device=dev)  # read as uint32 on device
         self.target_dof = torch.full((N,), -1, dtype=torch.int32, device=dev)
+        self.ep_return = torch.zeros(N, dtype=torch.float64, device=dev)
+        self.ep_flags = torch.zeros(N, dtype=torch.uint8, device=dev)
         # dof / actor validity masks
         ndof = torch.as_tensor([self.models[m].D for m in self.model_index], device=dev)
         nact = torch.as_tensor([self.models[m].A for m in self.model_index], device=dev)
@@ -319,12 +321,12 @@ class SceneBatch:
         cs = cabi.BsEnvState()
         cs.num_envs, cs.env_offset = N, self.env_offset
         for k in ("model_id", "qpos", "qvel", "target", "actor_pose", "actor_vel", "link_pose", "goal",
-                  "diverged", "elapsed", "reset_count", "target_dof"):
+                  "diverged", "elapsed", "reset_count", "target_dof", "ep_return", "ep_flags"):
             setattr(cs, k, getattr(self, k).data_ptr())
         self.c_state = cs
 
     STATE_FIELDS = ("qpos", "qvel", "target", "actor_pose", "actor_vel", "link_pose", "goal", "diverged",
-                    "elapsed", "reset_count", "target_dof")
+                    "elapsed", "reset_count", "target_dof", "ep_return", "ep_flags")
 
     def forward_kinematics(self):
         nat.call("bs_forward_kinematics", ctypes.byref(self.c_tables), ctypes.byref(self.c_state),

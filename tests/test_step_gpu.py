@@ -240,3 +240,36 @@ def test_ee_delta_pose_one_step_parity(cuda):
         tg = env.scene.target.cpu().numpy()[:, :3]
         assert np.isfinite(tg).all()
         compare(gpu_snapshot(env), orc.snapshot(), atol=1e-9, what=f"ee step {t}")
+
+
+def test_episode_metrics_match_oracle(cuda):
+    """In-kernel EpisodeMetrics vs the oracle accumulator on short episodes:
+    done masks, lengths and flags bit-exact; returns within 1e-6 relative."""
+    from oracle.metrics import EpisodeAccumulator
+    from oracle.philox import action_uniforms
+    from oracle.tasks import PickCubeOracle
+    from paper_2410_00425_b200.metrics import EpisodeStats
+    from paper_2410_00425_b200.tasks import make_task, pickcube_scene
+
+    env = make_task("PickCube", N, seed=21, overrides={"max_steps": 4})
+    orc = PickCubeOracle(env.spec, pickcube_scene(env.spec), N, 21)
+    acc = EpisodeAccumulator(N)
+    stats = EpisodeStats(env.device)
+    episodes = 0
+    for t in range(13):
+        r = env.step_random(t)
+        stats.update(r.info)
+        _, o_rew, o_term, o_trunc, o_info, final = orc.step(action_uniforms(21, t, np.arange(N), 3))
+        done, ret, length, flags = acc.update(o_rew, o_info["success"], o_info["fail"], o_term, o_trunc,
+                                              final["elapsed"])
+        ep = r.info["episode"]
+        g_done = ep["done"].cpu().numpy().astype(bool)
+        assert np.array_equal(g_done, done), t
+        if done.any():
+            assert np.array_equal(ep["length"].cpu().numpy()[done], length[done])
+            assert np.array_equal(ep["flags"].cpu().numpy()[done], flags[done])
+            g_ret = ep["return"].cpu().numpy()[done]
+            assert np.abs(g_ret - ret[done]).max() <= 1e-6 * (1 + np.abs(ret[done]).max())
+            episodes += int(done.sum())
+    assert episodes >= 3 * N
+    assert int(stats.sums[0]) == episodes
