@@ -1006,7 +1006,8 @@ static int launch(const BsModelTables& T, const BsEnvState& S, const BsStepOutpu
 }
 
 typedef Cfg<8, 4, 1> CfgSmall;    // PickCube-style: D <= 4, one free actor
-typedef Cfg<8, 12, 4> CfgLarge;   // cabinets / heterogeneous scenes
+typedef Cfg<8, 12, 1> CfgArt;     // articulated objects (arm + cabinet): D <= 12, <= 1 actor
+typedef Cfg<8, 12, 4> CfgLarge;   // general scenes: D <= 12, <= 4 actors
 
 }  // namespace step
 }  // namespace bs
@@ -1023,6 +1024,7 @@ int bs_step(const BsModelTables* T, const BsEnvState* S, const BsStepOutputs* O,
     return BS_ERR_ARGUMENT;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (T->D_max <= CfgSmall::MD && T->A_max <= CfgSmall::MA) return launch<CfgSmall>(*T, *S, *O, *P, action, st);
+  if (T->D_max <= CfgArt::MD && T->A_max <= CfgArt::MA) return launch<CfgArt>(*T, *S, *O, *P, action, st);
   if (T->D_max <= CfgLarge::MD && T->A_max <= CfgLarge::MA) return launch<CfgLarge>(*T, *S, *O, *P, action, st);
   return BS_ERR_UNSUPPORTED;
 }
