@@ -13,6 +13,7 @@ def test_library_built():
 
 def test_exports_every_header_symbol():
     lib = ctypes.CDLL(_native.LIB_PATH)
+    _native.load()  # binds the struct-taking entry points too (cabi)
     declared = _native.header_symbols()
     assert len(declared) >= 12
     missing = [s for s in declared if not hasattr(lib, s)]
