@@ -276,6 +276,21 @@ int bs_render(const BsModelTables* tables, const BsEnvState* state, const BsMesh
               const BsCameraBatch* cams, const float* env_color, const BsRenderParams* params,
               const BsFrameBatch* out, void* stream);
 
+
+/* voxelize(points, cell, bounds): occupancy grid [batches][nx][ny][nz] u8 of
+ * points (xyz at the start of each `point_stride`-float record, e.g. the fused pointcloud with
+ * stride 6), cell index = floor((p - lo) / cell) per axis in float32; points with valid == 0
+ * (may be NULL) or outside the grid are dropped.  `lo` is a HOST array of 3 floats.  cell <= 0
+ * -> BS_ERR_INPUT. */
+int bs_voxelize(const float* points, int64_t point_stride, const uint8_t* valid, int64_t points_per_batch,
+                int64_t batches, const float* lo, float cell, int32_t nx, int32_t ny, int32_t nz,
+                uint8_t* grid, void* stream);
+
+/* composite_greenscreen(frame, background): out = rgb where seg != 0, else the
+ * background pixel; rgb/out [frames][H][W][3] u8, seg [frames][H][W] u16, background [H][W][3]. */
+int bs_composite_greenscreen(const uint8_t* rgb, const uint16_t* seg, const uint8_t* background,
+                             int64_t height, int64_t width, int64_t frames, uint8_t* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -179,3 +179,20 @@ def pointcloud(depth, seg, rgb, cam_p, cam_q, intr, W, H):
     out = np.concatenate([pw, c], -1).astype(F)
     out[~valid] = 0
     return out
+
+
+def voxelize(points, valid, lo, cell, dims):
+    """SPEC.md:477-485 brute-force binning: cell = floor((p - lo) / cell) per axis (float32)."""
+    pts = np.asarray(points, F)
+    lo = np.asarray(lo, F)
+    idx = np.floor((pts[..., :3] - lo) / F(cell)).astype(np.int64)
+    grid = np.zeros(tuple(dims), np.uint8)
+    ok = np.ones(len(pts), bool) if valid is None else np.asarray(valid, bool)
+    ok &= (idx >= 0).all(-1) & (idx < np.asarray(dims)).all(-1)
+    grid[idx[ok, 0], idx[ok, 1], idx[ok, 2]] = 1
+    return grid
+
+
+def composite_greenscreen(rgb, seg, background):
+    """rendered pixel where seg != 0, else the background pixel."""
+    return np.where((np.asarray(seg) != 0)[..., None], rgb, background).astype(np.uint8)

@@ -34,6 +34,7 @@ SOURCES = {
     "sim.cu": [],
     "step.cu": [],
     "raster.cu": NOFMA,
+    "vision_ops.cu": NOFMA,
     "capi.cu": [],
 }
 

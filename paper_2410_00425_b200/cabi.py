@@ -71,6 +71,8 @@ _native.register("bs_reset", [_R(BsModelTables), _R(BsEnvState), _R(BsStepOutput
 _native.register("bs_forward_kinematics", [_R(BsModelTables), _R(BsEnvState), P])
 _native.register("bs_random_actions", [ctypes.c_uint64, I64, I64, I32, I32, P, P])
 _native.register("bs_masked_copy", [P, P, I64, I64, P, P])
+_native.register("bs_voxelize", [P, I64, P, I64, I64, P, F32, I32, I32, I32, P, P])
+_native.register("bs_composite_greenscreen", [P, P, P, I64, I64, I64, P, P])
 _native.register("bs_render", [_R(BsModelTables), _R(BsEnvState), _R(BsMeshTables), _R(BsCameraBatch), P,
                                _R(BsRenderParams), _R(BsFrameBatch), P])
 

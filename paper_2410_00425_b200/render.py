@@ -157,3 +157,41 @@ class Renderer:
         keep = {"rgb": ("rgb",), "depth": ("depth",), "rgbd": ("rgb", "depth"), "rgb+depth": ("rgb", "depth"),
                 "seg": ("seg",)}[mode]
         return {"sensor_data": {name: {k: f[k] for k in keep + ("seg",)} for name, f in fr.items()}}
+
+
+def voxelize(points: torch.Tensor, cell: float, lo, dims, valid: torch.Tensor = None) -> torch.Tensor:
+    """occupancy grid (B, nx, ny, nz) u8 of (B, P, >=3) float32 points (e.g. the
+    fused pointcloud) -- a cell is occupied iff >= 1 (valid) point falls inside."""
+    if not cell > 0:
+        raise InputError("voxel cell size must be positive")
+    pts = points.contiguous()
+    if pts.dtype != torch.float32 or pts.dim() != 3 or pts.shape[-1] < 3:
+        raise DimensionError("points must be (B, P, >=3) float32")
+    B, Pn, stride = pts.shape
+    nx, ny, nz = (int(d) for d in dims)
+    grid = torch.empty((B, nx, ny, nz), dtype=torch.uint8, device=pts.device)
+    v = None
+    if valid is not None:
+        v = valid.to(torch.uint8).contiguous()
+        if v.shape != (B, Pn):
+            raise DimensionError(f"valid must be ({B}, {Pn})")
+    lo_c = (ctypes.c_float * 3)(*[float(x) for x in lo])
+    nat.call("bs_voxelize", nat.ptr(pts), stride, None if v is None else v.data_ptr(), Pn, B, lo_c, float(cell),
+             nx, ny, nz, grid.data_ptr(), nat.stream_handle())
+    return grid
+
+
+def composite_greenscreen(rgb: torch.Tensor, seg: torch.Tensor, background) -> torch.Tensor:
+    """rendered rgb where seg != 0, else the background image (H, W, 3) u8."""
+    bg = torch.as_tensor(background, dtype=torch.uint8, device=rgb.device).contiguous()
+    H, W = rgb.shape[-3], rgb.shape[-2]
+    if bg.shape != (H, W, 3):
+        raise DimensionError(f"background must be ({H}, {W}, 3), got {tuple(bg.shape)}")
+    if seg.shape != rgb.shape[:-1]:
+        raise DimensionError("seg must match rgb's (..., H, W)")
+    rgb_c, seg_c = rgb.contiguous(), seg.contiguous()
+    out = torch.empty_like(rgb_c)
+    frames = rgb_c.numel() // (H * W * 3)
+    nat.call("bs_composite_greenscreen", rgb_c.data_ptr(), seg_c.data_ptr(), bg.data_ptr(), H, W, frames,
+             out.data_ptr(), nat.stream_handle())
+    return out

@@ -82,3 +82,30 @@ def test_nearest_wins_and_ties_to_lower_triangle():
         np.ones((2, 3), np.float32), np.array([0, 0, -1.0]), 0.3, 0.7, (0, 0, 0))
     assert seg[32, 32] == 3 and abs(depth[32, 32] - 1.7) < 1e-3
     assert seg[32, 20] == 9 and abs(depth[32, 20] - 2.9) < 1e-3
+
+
+def test_voxelize_kats():
+    # empty cloud -> empty grid; occupancy == brute-force binning
+    assert raster.voxelize(np.zeros((0, 3)), None, (0, 0, 0), 0.1, (4, 4, 4)).sum() == 0
+    rng = np.random.default_rng(0)
+    pts = rng.uniform(-0.1, 0.5, (500, 3)).astype(np.float32)
+    g = raster.voxelize(pts, None, (0.0, 0.0, 0.0), 0.1, (4, 4, 4))
+    want = np.zeros((4, 4, 4), np.uint8)
+    for p in pts:
+        i = np.floor(p / np.float32(0.1)).astype(int)
+        if (i >= 0).all() and (i < 4).all():
+            want[tuple(i)] = 1
+    assert np.array_equal(g, want)
+
+
+def test_greenscreen_kats():
+    # empty scene -> background; full cover -> rendered; provenance == seg mask
+    rng = np.random.default_rng(1)
+    bg = rng.integers(0, 256, (8, 8, 3), dtype=np.uint8)
+    rgb = rng.integers(0, 256, (8, 8, 3), dtype=np.uint8)
+    assert np.array_equal(raster.composite_greenscreen(rgb, np.zeros((8, 8)), bg), bg)
+    assert np.array_equal(raster.composite_greenscreen(rgb, np.ones((8, 8)), bg), rgb)
+    seg = np.zeros((8, 8))
+    seg[:, :4] = 3
+    out = raster.composite_greenscreen(rgb, seg, bg)
+    assert np.array_equal(out[:, :4], rgb[:, :4]) and np.array_equal(out[:, 4:], bg[:, 4:])

@@ -146,3 +146,28 @@ def test_spec_kat_wall_pointcloud(cuda):
     R.render()
     pc = R.frames()["c"]["pointcloud"].cpu().numpy()[0]
     assert np.abs(pc[:, 2] - 2.0).max() < 1e-3
+
+
+def test_voxelize_and_greenscreen_match_oracle(cuda):
+    from oracle import raster
+    from paper_2410_00425_b200.render import composite_greenscreen, voxelize
+    from paper_2410_00425_b200.tasks import make_task
+
+    env = make_task("PickCube", 3, seed=9, obs_mode="pointcloud")
+    obs = env.step_random(0).obs
+    pc, mask = obs["pointcloud"], obs["pointcloud_mask"]
+    grid = voxelize(pc, 0.05, (-1.0, -1.0, -0.05), (40, 40, 12), valid=mask).cpu().numpy()
+    pcn, mn = pc.cpu().numpy(), mask.cpu().numpy()
+    for e in range(3):
+        want = raster.voxelize(pcn[e], mn[e], (-1.0, -1.0, -0.05), 0.05, (40, 40, 12))
+        assert np.array_equal(grid[e], want), e
+        assert grid[e].sum() > 10
+    with pytest.raises(Exception):
+        voxelize(pc, 0.0, (0, 0, 0), (2, 2, 2))
+    # green screen over real frames
+    env2 = make_task("PickCube", 2, seed=9, obs_mode="rgbd")
+    cam = env2.step_random(0).obs["sensor_data"]["base_camera"]
+    bg = np.random.default_rng(0).integers(0, 256, (128, 128, 3), dtype=np.uint8)
+    out = composite_greenscreen(cam["rgb"], cam["seg"], bg).cpu().numpy()
+    want = raster.composite_greenscreen(cam["rgb"].cpu().numpy(), cam["seg"].cpu().numpy(), bg)
+    assert np.array_equal(out, want)
