@@ -118,4 +118,8 @@ def make_task(name: str, num_envs: int, seed: int = 0, overrides=None, obs_mode:
         raise KeyError(f"unknown task {name!r}; registered: {sorted(TASKS)}")
     if num_envs < 1:
         raise ValueError("num_envs must be >= 1")
-    return TASKS[name](num_envs, seed, overrides, obs_mode, device, shard, sim, cameras, **kw)
+    env = TASKS[name](num_envs, seed, overrides, obs_mode, device, shard, sim, cameras, **kw)
+    env.task_name = name
+    env.overrides = dict(overrides or {})
+    env.global_num_envs = num_envs
+    return env
