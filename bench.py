@@ -124,6 +124,17 @@ class ClockSampler:
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": rows[0][1], "reasons": reasons, "samples": len(rows)}
 
 
+def _traffic(kernel: str, workload: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` on `workload`, from the
+    committed ncu --set full capture summary (profiles/traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        return t.get(workload, {}).get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
 def sim_bytes_per_env_step(scene, obs_dim, action_dim):
     """Bytes the fused step must move per env-step.
 
@@ -390,7 +401,7 @@ def run_workload(name, steps, warmup, world, rank, local, dist, flush, seed, e2e
             dominant = "k_render"
     dk = kernels[dominant]
     roof = {"bound": "hbm", "achieved": dk["achieved_gbs"], "peak": peak, "unit": "GB/s",
-            "frac": dk["achieved_gbs"] / peak, "traffic": None, "kernel": dominant,
+            "frac": dk["achieved_gbs"] / peak, "traffic": _traffic(dominant, name), "kernel": dominant,
             "bytes_per_env_step": dk["bytes_per_env_step"], "kernel_us_per_launch": dk["us_per_launch"],
             "peak_source": peak_kind, "kernels": kernels}
     line = {"metric": METRIC, "value": value, "unit": "env-steps/s", "n_gpus": world, "steps": steps,
