@@ -263,7 +263,7 @@ __device__ int narrow_pair(const Model& M, int pi, const R* spq, R slop, R* cand
 // Lanes build each link's local transform (joint origin o joint motion, with the sincos),
 // then lane 0 walks the topological order composing parent o local.
 template <int G>
-__device__ __noinline__ void fk_group(const Model& M, const Lay& Y, R* E, int l) {
+__device__ __forceinline__ void fk_group(const Model& M, const Lay& Y, R* E, int l) {
   R* Tl = E + Y.Tl;
   R* lpq = E + Y.lpq;
   #pragma unroll 1
