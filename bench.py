@@ -323,39 +323,32 @@ def measure(env, steps, warmup, flush, dist, local, seed_step=0):
 
 
 def measure_e2e(env, steps, dist, seed):
-    """The public API with host buffers: Env.step(pinned host action) + D2H of obs and reward."""
+    """The public API with host buffers: Env.step_host(host action) -- one CUDA graph with the
+    H2D copy of the action, the step (+ render) and the D2H copies of every obs tensor, the
+    reward and the flags -- then a stream synchronisation, every step."""
     import numpy as np
     import torch
 
     N = env.num_envs
-    stream = torch.cuda.current_stream(env.device)
     rng = np.random.default_rng(seed)
-    host_actions = torch.from_numpy(rng.uniform(-1, 1, (steps, N, env.action_dim)).astype(np.float32)).pin_memory()
-    obs0 = env.step(host_actions[0]).obs
-    flat = {"state": obs0} if not isinstance(obs0, dict) else _flatten(obs0)
-    hosts = {k: torch.empty(v.shape, dtype=v.dtype).pin_memory() for k, v in flat.items()}
-    rew_host = torch.empty((N,), dtype=torch.float32).pin_memory()
-    d2h = sum(v.numel() * v.element_size() for v in flat.values()) + N * 4
-    env.capture_graph()
+    host_actions = rng.uniform(-1, 1, (steps, N, env.action_dim)).astype(np.float32)
+    env.enable_host_io()
     for k in range(3):
-        env.step(host_actions[k])
+        env.step_host(host_actions[k])
+    h2d, d2h = env.host_io_bytes()
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
     t0 = time.perf_counter()
     for k in range(steps):
-        r = env.step(host_actions[k])                 # H2D of the action inside
-        cur = {"state": r.obs} if not isinstance(r.obs, dict) else _flatten(r.obs)
-        for name, v in cur.items():
-            hosts[name].copy_(v, non_blocking=True)   # D2H of the step's results
-        rew_host.copy_(r.reward, non_blocking=True)
-        stream.synchronize()
+        out = env.step_host(host_actions[k])
+        _ = out["reward"]
     e2e_s = time.perf_counter() - t0
     if dist is not None:
         tt = torch.tensor([e2e_s], dtype=torch.float64, device=env.device)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt[0])
-    return e2e_s, N * env.action_dim * 4, d2h
+    return e2e_s, h2d, d2h
 
 
 def _flatten(d, prefix=""):
@@ -386,7 +379,8 @@ def run_workload(name, steps, warmup, world, rank, local, dist, flush, seed, e2e
     e2e_s, h2d, d2h = measure_e2e(env, e2e_steps, dist, seed + rank)
     e2e = {"value": n_global * e2e_steps / e2e_s, "unit": "env-steps/s", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h, "steps": e2e_steps,
-           "path": "Env.step(pinned host action) + every obs tensor and the reward D2H, CUDA graph"}
+           "path": "Env.step_host: one CUDA graph per step = H2D action + step (+ render) + D2H of every obs "
+                   "tensor, reward and flags; stream sync every step"}
     peak, peak_kind = _peaks()
     sim_b = sim_bytes_per_env_step(env.scene, env.obs_dim, env.action_dim)
     sim_s = m["sim_ms"] / 1e3 / steps

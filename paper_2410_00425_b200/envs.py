@@ -222,6 +222,70 @@ class Env:
         self.scene.set_state(snap)
         self._graph = g
 
+    # ------------------------------------------------------------------ host I/O path
+    def enable_host_io(self, warmup: int = 2) -> None:
+        """Capture [H2D action, step, render, D2H obs/reward/flags] as ONE CUDA graph over pinned
+        host staging buffers, for callers that keep actions and observations on the host
+        (``step_host``).  The device-side API (``step``) is unaffected."""
+        N, A = self.num_envs, max(1, self.action_dim)
+        self._h_action = torch.zeros((N, A), dtype=torch.float32).pin_memory()
+        outs = self._host_outputs()
+        self._h_outs = {k: torch.empty(v.shape, dtype=v.dtype).pin_memory() for k, v in outs.items()}
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        snap = self.scene.get_state()
+        with torch.cuda.stream(s):
+            for _ in range(warmup):
+                self._launch_step(self.action_buf.data_ptr())
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.action_buf.copy_(self._h_action, non_blocking=True)
+            self._launch_step(self.action_buf.data_ptr())
+            for k, v in outs.items():
+                self._h_outs[k].copy_(v, non_blocking=True)
+        self.scene.set_state(snap)
+        self._host_graph = g
+
+    def _host_outputs(self) -> dict:
+        out = {"reward": self.reward, "terminated": self.terminated, "truncated": self.truncated,
+               "success": self.success, "fail": self.fail}
+        o = self._obs()
+        if isinstance(o, dict):
+            def walk(d, prefix=""):
+                for k, v in d.items():
+                    if isinstance(v, dict):
+                        walk(v, prefix + k + "/")
+                    else:
+                        out["obs/" + prefix + k] = v
+            walk(o)
+        else:
+            out["obs"] = o
+        return out
+
+    def step_host(self, action):
+        """Host-resident step: `action` (N, D) array-like on the host -> dict of pinned host
+        tensors (obs..., reward, terminated, truncated, success, fail), valid until the next
+        call.  One graph launch and one stream synchronisation per step."""
+        import numpy as np
+
+        if getattr(self, "_host_graph", None) is None:
+            self.enable_host_io()
+        a = np.asarray(action, dtype=np.float32)
+        if a.shape != (self.num_envs, self.action_dim):
+            raise DimensionError(f"action must have shape ({self.num_envs}, {self.action_dim}), got {a.shape}")
+        if self.validate_actions and not np.isfinite(a).all():
+            raise InputError("non-finite action")
+        self._h_action.numpy()[:, :self.action_dim] = a
+        self._host_graph.replay()
+        torch.cuda.current_stream(self.device).synchronize()
+        return self._h_outs
+
+    def host_io_bytes(self):
+        """(H2D, D2H) bytes per step_host call."""
+        return (self._h_action.numel() * 4,
+                sum(v.numel() * v.element_size() for v in self._h_outs.values()))
+
     def _obs(self):
         if self.obs_mode == "state":
             return self.state_obs

@@ -273,3 +273,22 @@ def test_episode_metrics_match_oracle(cuda):
             episodes += int(done.sum())
     assert episodes >= 3 * N
     assert int(stats.sums[0]) == episodes
+
+
+def test_step_host_matches_device_step(cuda):
+    """Env.step_host (one graph: H2D action, step, render, D2H outputs) == Env.step."""
+    from paper_2410_00425_b200.tasks import make_task
+
+    a = make_task("PickCube", 8, seed=17, obs_mode="rgbd")
+    b = make_task("PickCube", 8, seed=17, obs_mode="rgbd")
+    rng = np.random.default_rng(2)
+    for t in range(6):
+        act = rng.uniform(-1, 1, (8, 3)).astype(np.float32)
+        ra = a.step(torch.as_tensor(act, device=a.device))
+        hb = b.step_host(act)
+        assert np.array_equal(ra.reward.cpu().numpy(), hb["reward"].numpy())
+        assert np.array_equal(ra.obs["state"].cpu().numpy(), hb["obs/state"].numpy())
+        assert np.array_equal(ra.obs["sensor_data"]["base_camera"]["rgb"].cpu().numpy(),
+                              hb["obs/sensor_data/base_camera/rgb"].numpy())
+    h2d, d2h = b.host_io_bytes()
+    assert h2d == 8 * 3 * 4 and d2h > 8 * 128 * 128 * 3
