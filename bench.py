@@ -286,6 +286,16 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------------------ GPU path
+def _allreduce(dist, t, op):
+    """All-reduce in place; through host memory when the backend cannot reduce CUDA tensors."""
+    if dist.get_backend() == "nccl":
+        dist.all_reduce(t, op=op)
+    else:
+        h = t.cpu()
+        dist.all_reduce(h, op=op)
+        t.copy_(h)
+
+
 def measure(env, steps, warmup, flush, dist, local, seed_step=0):
     """Device timing of `steps` env steps: per step, flush L2 (untimed), then events around
     the random-action launch, the fused step and the render."""
@@ -316,7 +326,7 @@ def measure(env, steps, warmup, flush, dist, local, seed_step=0):
     t = torch.tensor([sum(e[0].elapsed_time(e[3]) for e in ev), sum(e[1].elapsed_time(e[2]) for e in ev),
                       sum(e[2].elapsed_time(e[3]) for e in ev)], dtype=torch.float64, device=env.device)
     if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        _allreduce(dist, t, dist.ReduceOp.MAX)
     launches = 2 + (len(env.renderer.groups) if env.renderer is not None else 0)
     return {"step_ms": float(t[0]), "sim_ms": float(t[1]), "render_ms": float(t[2]), "clocks": clk.summary(),
             "launches": launches * steps}
@@ -346,7 +356,7 @@ def measure_e2e(env, steps, dist, seed):
     e2e_s = time.perf_counter() - t0
     if dist is not None:
         tt = torch.tensor([e2e_s], dtype=torch.float64, device=env.device)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        _allreduce(dist, tt, dist.ReduceOp.MAX)
         e2e_s = float(tt[0])
     return e2e_s, h2d, d2h
 
@@ -375,7 +385,7 @@ def run_workload(name, steps, warmup, world, rank, local, dist, flush, seed, e2e
     value = n_global * steps / (m["step_ms"] / 1e3)
     stats = torch.stack([env.success.sum().double(), env.terminated.sum().double(), env.truncated.sum().double()])
     if dist is not None:
-        dist.all_reduce(stats)  # rollout statistics: the only data collective
+        _allreduce(dist, stats, dist.ReduceOp.SUM)  # rollout statistics: the only data collective
     e2e_s, h2d, d2h = measure_e2e(env, e2e_steps, dist, seed + rank)
     e2e = {"value": n_global * e2e_steps / e2e_s, "unit": "env-steps/s", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h, "steps": e2e_steps,
@@ -436,12 +446,17 @@ def run_ours(args):
                                               obs_mode=w2["obs_mode"])
             cpu2 = {"value": rate, "unit": "env-steps/s", "cores": cores, "kind": "port", "sample": info}
 
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")  # gloo: multi-rank smoke on one GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_2410_00425_b200 import _native as nat
 
     nat.ensure_device(local)

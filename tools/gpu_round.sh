@@ -11,6 +11,8 @@ fi
 for c in c4 c5; do
   timeout 300 python bench.py --config $c --steps 30 --warmup 3 --no-cpu --secondary "" > gpurun_out/${TAG}_bench_$c.json 2>> gpurun_out/${TAG}_bench.err
 done
+# multi-rank code path (2 ranks sharing this one GPU, gloo for the statistics collectives)
+BENCH_DIST_BACKEND=gloo timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 10 --warmup 3 --no-cpu --secondary "" > gpurun_out/${TAG}_bench_2rank.json 2>> gpurun_out/${TAG}_bench.err
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 5 --warmup 3 --no-cpu > /dev/null 2>> gpurun_out/${TAG}_ncu.err
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_step -s 3 -c 1 -o gpurun_out/${TAG}_prof_step python bench.py --steps 3 --warmup 3 --no-cpu --secondary "" > /dev/null 2>> gpurun_out/${TAG}_ncu.err
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_render -s 3 -c 1 -o gpurun_out/${TAG}_prof_render python bench.py --config c3 --steps 3 --warmup 3 --no-cpu --secondary "" > /dev/null 2>> gpurun_out/${TAG}_ncu.err
