@@ -154,11 +154,13 @@ int quat_normalize_impl(const R* q, int64_t n, R* out, void* stream) {
 template <typename R>
 int compose_impl(const R* pa, const R* qa, int64_t na, const R* pb, const R* qb, int64_t nb,
                  R* po, R* qo, void* stream) {
-  if (na < 1 || nb < 1) return BS_ERR_DIMENSION;
+  if (na < 0 || nb < 0) return BS_ERR_ARGUMENT;
   if (na != nb && na != 1 && nb != 1) return BS_ERR_DIMENSION;
+  // pose.py:167-174: equal sizes, or a singleton side broadcast to the other (also to 0)
+  const int64_t n = na == nb ? na : (na == 1 ? nb : na);
+  if (n == 0) return BS_OK;
   BS_CHECK_PTR(pa); BS_CHECK_PTR(qa); BS_CHECK_PTR(pb); BS_CHECK_PTR(qb);
   BS_CHECK_PTR(po); BS_CHECK_PTR(qo);
-  int64_t n = na > nb ? na : nb;
   k_pose_compose<R><<<grid_for(n, 256), 256, 0, BS_STREAM(stream)>>>(pa, qa, na, pb, qb, nb, n,
                                                                         po, qo);
   return launch_status();
@@ -176,10 +178,10 @@ int inverse_impl(const R* p, const R* q, int64_t n, R* po, R* qo, void* stream) 
 template <typename R>
 int transform_points_impl(const R* p, const R* q, int64_t n, const R* pts, int64_t m, int64_t k,
                           R* out, void* stream) {
-  if (n < 1 || m < 1 || k < 0) return BS_ERR_DIMENSION;
+  if (n < 0 || m < 0 || k < 0) return BS_ERR_ARGUMENT;
   if (n != m && n != 1 && m != 1) return BS_ERR_DIMENSION;
-  int64_t nout = n > m ? n : m;
-  if (k == 0) return BS_OK;
+  const int64_t nout = n == m ? n : (n == 1 ? m : n);  // singleton broadcast, also to 0
+  if (k == 0 || nout == 0) return BS_OK;
   BS_CHECK_PTR(p); BS_CHECK_PTR(q); BS_CHECK_PTR(pts); BS_CHECK_PTR(out);
   k_pose_transform_points<R><<<grid_for(nout * k, 256), 256, 0, BS_STREAM(stream)>>>(
       p, q, n, pts, m, k, nout, out);

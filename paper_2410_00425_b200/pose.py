@@ -60,8 +60,13 @@ def quat_conjugate(q: torch.Tensor) -> torch.Tensor:
 
 
 def _check_pair(na: int, nb: int) -> int:
-    if na == nb or na == 1 or nb == 1:
-        return max(na, nb)
+    # pose.py:167-174: equal sizes, or a singleton side broadcast to the other (incl. 0)
+    if na == nb:
+        return na
+    if na == 1:
+        return nb
+    if nb == 1:
+        return na
     raise DimensionError(f"incompatible batch sizes {na} and {nb}")
 
 
@@ -230,7 +235,7 @@ class PoseBatch:
             raise DimensionError(
                 f"points batch {pts.shape[0]} incompatible with pose batch {len(self)}")
         pts = pts.contiguous()
-        n = max(len(self), pts.shape[0])
+        n = _check_pair(len(self), pts.shape[0])
         out = torch.empty((n, pts.shape[1], 3), dtype=self.dtype, device=self.p.device)
         nat.call(f"bs_pose_transform_points_{_SUFFIX[self.dtype]}", nat.ptr(self.p),
                  nat.ptr(self.q), len(self), nat.ptr(pts), pts.shape[0], pts.shape[1],
