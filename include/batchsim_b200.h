@@ -95,7 +95,8 @@ enum { BS_BODY_LINK = 0, BS_BODY_ACTOR = 1, BS_BODY_STATIC = 2 };
 enum { BS_PAIR_UNSUPPORTED = 0, BS_PAIR_SPHERE_PLANE = 1, BS_PAIR_BOX_PLANE = 2,
        BS_PAIR_SPHERE_SPHERE = 3, BS_PAIR_SPHERE_BOX = 4, BS_PAIR_CAPSULE_PLANE = 5,
        BS_PAIR_SWAP = 16 };
-enum { BS_CTRL_PD_JOINT_POS = 0, BS_CTRL_PD_JOINT_DELTA_POS = 1, BS_CTRL_PD_EE_DELTA_POSE = 2 };
+enum { BS_CTRL_PD_JOINT_POS = 0, BS_CTRL_PD_JOINT_DELTA_POS = 1, BS_CTRL_PD_EE_DELTA_POSE = 2,
+       BS_CTRL_BASE_FORWARD_ROTATE = 3 };
 enum { BS_TASK_NONE = 0, BS_TASK_PICKCUBE = 1, BS_TASK_OPENCHAIN = 2 };
 
 typedef struct BsModelTables {

@@ -239,6 +239,16 @@ def controller_targets(model, ctrl, q, action):
         twist = np.concatenate([a[:, :3] * ctrl.scale, a[:, 3:6] * ctrl.rot_scale], -1)
         dq = ik_delta(J, twist, ctrl.lam)
         tgt[:, dofs] = np.clip(q[:, dofs] + dq, lo, hi)
+    elif ctrl.mode == "base_forward_rotate":
+        # controlled dofs 0,1,2 = base x, y, yaw; (forward, rotate) ->
+        # planar targets one control step ahead along the current heading
+        a0, a1 = a[:, 0], a[:, 1]
+        dx, dy, dyaw = dofs[0], dofs[1], dofs[2]
+        yaw = q[:, dyaw]
+        step = a0 * ctrl.scale
+        tgt[:, dx] = np.clip(q[:, dx] + step * np.cos(yaw), model.lower[dx], model.upper[dx])
+        tgt[:, dy] = np.clip(q[:, dy] + step * np.sin(yaw), model.lower[dy], model.upper[dy])
+        tgt[:, dyaw] = np.clip(yaw + a1 * ctrl.rot_scale, model.lower[dyaw], model.upper[dyaw])
     else:
         raise NotImplementedError(ctrl.mode)
     return tgt

@@ -800,6 +800,27 @@ __global__ void __launch_bounds__(32) k_step(BsModelTables T, BsEnvState S, BsSt
     __syncwarp();
     fk_group<G>(M, Y, E, l);
     if (l == 0) ee_delta_targets(M, P, Y, E, act);
+  } else if (P.ctrl_mode == BS_CTRL_BASE_FORWARD_ROTATE) {
+    // mobile base: controlled dofs 0, 1, 2 = base x, y, yaw; the action
+    // (forward, rotate) in [-1, 1] becomes planar targets one control step ahead along the
+    // current heading: x* = x + a0 s cos(yaw), y* = y + a0 s sin(yaw), yaw* = yaw + a1 s_rot
+    __syncwarp();  // E[q] is staged by the other lanes
+    if (l == 0) {
+      int bd[3] = {-1, -1, -1};
+      for (int d = 0; d < M.D; ++d) {
+        const int c = M.ctrl[d];
+        if (c == 0) bd[0] = d; else if (c == 1) bd[1] = d; else if (c == 2) bd[2] = d;
+      }
+      const R a0 = fmin(fmax((R)act[0], -1.0), 1.0), a1 = fmin(fmax((R)act[1], -1.0), 1.0);
+      const R yaw = bd[2] >= 0 ? E[Y.q + bd[2]] : 0.0;
+      R sy, cy;
+      sincos(yaw, &sy, &cy);
+      for (int d = 0; d < M.D; ++d) E[Y.tgt + d] = E[Y.q + d];
+      const R stp = a0 * P.action_scale;
+      if (bd[0] >= 0) E[Y.tgt + bd[0]] = fmin(fmax(E[Y.q + bd[0]] + stp * cy, M.lower[bd[0]]), M.upper[bd[0]]);
+      if (bd[1] >= 0) E[Y.tgt + bd[1]] = fmin(fmax(E[Y.q + bd[1]] + stp * sy, M.lower[bd[1]]), M.upper[bd[1]]);
+      if (bd[2] >= 0) E[Y.tgt + bd[2]] = fmin(fmax(yaw + a1 * P.action_scale_rot, M.lower[bd[2]]), M.upper[bd[2]]);
+    }
   } else {
     #pragma unroll 1
     for (int i = l; i < M.D; i += G) {

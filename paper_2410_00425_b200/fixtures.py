@@ -200,3 +200,20 @@ def make_cabinet_urdf(kinds: str, name: str = "cabinet") -> str:
             joints.append(_joint(f"door{i}_joint", "revolute", "carcass", f"door{i}", axis="0 0 1",
                                  xyz=f"0.16 0.2 {zc:.3f}", limit=("0", "1.5"), damping="0.5"))
     return _robot(name, links, joints)
+
+
+def make_mobile_base_urdf(name: str = "mobile_base") -> str:
+    """Abstract mobile base for the ``base_forward_rotate`` controller (PAPER §A.2:
+    "one joint controlling forward/backward movement and another controlling rotation"):
+    world-fixed root -> prismatic x -> prismatic y -> revolute yaw -> box chassis.  The
+    controller drives the planar joints kinematically from (forward speed, yaw rate)."""
+    links = [_link("odom"),
+             _link("base_x", _inertial("5.0", ("0.05", "0.05", "0.05"))),
+             _link("base_y", _inertial("5.0", ("0.05", "0.05", "0.05"))),
+             _link("chassis", _inertial("10.0", ("0.2", "0.3", "0.4")),
+                   _collision('<box size="0.5 0.4 0.2"/>', xyz="0 0 0.3"), color="0.3 0.3 0.35 1")]
+    joints = [_joint("base_x_joint", "prismatic", "odom", "base_x", axis="1 0 0", limit=("-5", "5"), damping="1.0"),
+              _joint("base_y_joint", "prismatic", "base_x", "base_y", axis="0 1 0", limit=("-5", "5"), damping="1.0"),
+              _joint("base_yaw_joint", "revolute", "base_y", "chassis", axis="0 0 1", limit=("-1e9", "1e9"),
+                     damping="1.0")]
+    return _robot(name, links, joints)

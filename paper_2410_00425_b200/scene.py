@@ -165,7 +165,8 @@ class PackedModel:
                 self.ctrl[d] = n
                 self.kp[d], self.kd[d], self.flim[d] = control.kp, control.kd, control.force_limit
                 n += 1
-        self.action_dim = 6 if control.mode == "pd_ee_delta_pose" and n else n
+        self.action_dim = (6 if control.mode == "pd_ee_delta_pose" and n else
+                           2 if control.mode == "base_forward_rotate" and n else n)
 
 
 def _stack(models, fn, width, dtype, fill=0):

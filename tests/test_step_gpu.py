@@ -292,3 +292,41 @@ def test_step_host_matches_device_step(cuda):
                               hb["obs/sensor_data/base_camera/rgb"].numpy())
     h2d, d2h = b.host_io_bytes()
     assert h2d == 8 * 3 * 4 and d2h > 8 * 128 * 128 * 3
+
+
+def test_base_forward_rotate_matches_oracle(cuda):
+    """base_forward_rotate: 2-D action (forward, rotate) -> planar
+    targets of an abstract mobile base; device == oracle within 1e-9 and the base drives along
+    its heading."""
+    import math
+
+    from oracle import engine as E
+    from oracle.model import Model
+    from paper_2410_00425_b200 import cabi
+    from paper_2410_00425_b200.assets import load_urdf
+    from paper_2410_00425_b200.descriptors import GROUND, ArticulationDesc, ControlSpec, SceneDesc
+    from paper_2410_00425_b200.envs import Env
+    from paper_2410_00425_b200.fixtures import make_mobile_base_urdf
+    from paper_2410_00425_b200.scene import build_batch
+
+    desc = SceneDesc((ArticulationDesc("base", load_urdf(make_mobile_base_urdf())),), (), (GROUND,))
+    ctl = ControlSpec("base_forward_rotate", "base", action_scale=0.05, action_scale_rot=0.1)
+    scene = build_batch([desc] * 4, 0, ctl)
+    env = Env(scene, cabi.TASK_NONE, [0.0] * 9, -1, 1000, 0, name="DriveBase")
+    env.reset()
+    assert env.action_dim == 2
+    m = Model(desc)
+    drv = E.Drives(np.full(3, ctl.kp), np.full(3, ctl.kd), np.full(3, ctl.force_limit), np.zeros((4, 3)))
+    ctrl = type("C", (), {"mode": "base_forward_rotate", "dofs": [0, 1, 2], "scale": 0.05, "rot_scale": 0.1})()
+    rng = np.random.default_rng(5)
+    for t in range(10):
+        q0, qd0 = env.scene.qpos.cpu().numpy(), env.scene.qvel.cpu().numpy()
+        st = E.State(q0.copy(), qd0.copy(), np.zeros((4, 0, 3)), np.zeros((4, 0, 4)), np.zeros((4, 0, 3)),
+                     np.zeros((4, 0, 3)), np.zeros(4, np.uint8))
+        a = rng.uniform(-1, 1, (4, 2)).astype(np.float32)
+        a[:, 0] = 1.0
+        env.step(torch.as_tensor(a, device=env.device))
+        st = E.control_step(m, st, drv, ctrl, a, E.SimConfig())
+        assert np.abs(env.scene.qpos.cpu().numpy() - st.q).max() < 1e-9, t
+    q = env.scene.qpos.cpu().numpy()
+    assert (np.hypot(q[:, 0], q[:, 1]) > 0.05).all()  # moved forward along the heading
