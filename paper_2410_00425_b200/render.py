@@ -116,7 +116,10 @@ class Renderer:
         for i in range(3):
             rp.light_dir[i] = L[i]
             rp.background[i] = params.background[i]
-        rp.ambient, rp.diffuse, rp.tile = params.ambient, params.diffuse, params.tile
+        import os
+
+        rp.ambient, rp.diffuse = params.ambient, params.diffuse
+        rp.tile = int(os.environ.get("BS_RENDER_TILE", params.tile))  # CTA tile edge (perf knob)
         self.c_params = rp
         self.light = L
         self.env_color = None

@@ -72,3 +72,9 @@ def test_cabinet_family(kinds):
     t = A.load_urdf(F.make_cabinet_urdf(kinds))
     assert t.dof == len(kinds)
     assert [j.joint_type for j in t.joints] == ["prismatic" if k == "d" else "revolute" for k in kinds]
+
+
+def test_mobile_base_fixture():
+    t = A.load_urdf(F.make_mobile_base_urdf())
+    assert t.dof == 3
+    assert [j.joint_type for j in t.joints] == ["prismatic", "prismatic", "revolute"]
