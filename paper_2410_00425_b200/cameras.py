@@ -102,4 +102,4 @@ class RenderParams:
     ambient: float = 0.35
     diffuse: float = 0.65
     background: tuple = (0.0, 0.0, 0.0)
-    tile: int = 64
+    tile: int = 128
