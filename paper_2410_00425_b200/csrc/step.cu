@@ -21,6 +21,7 @@
 // sweep: rows carry 1/K and M^-1 is explicit (the oracle also forms inv(Mt)).  Nothing in the
 // step is a dense contraction, so there are no tensor cores; the kernel is latency/ALU
 // bound and moves ~0.8 KB of HBM per env-step.
+#include <stdlib.h>
 #include "sim_common.cuh"
 
 namespace bs {
@@ -1027,6 +1028,7 @@ static int launch(const BsModelTables& T, const BsEnvState& S, const BsStepOutpu
 }
 
 typedef Cfg<8, 4, 1> CfgSmall;    // PickCube-style: D <= 4, one free actor
+typedef Cfg<16, 4, 1> CfgSmall16; // same with 16 lanes per env (2 envs per warp), BS_STEP_LANES=16
 typedef Cfg<8, 12, 1> CfgArt;     // articulated objects (arm + cabinet): D <= 12, <= 1 actor
 typedef Cfg<8, 12, 4> CfgLarge;   // general scenes: D <= 12, <= 4 actors
 
@@ -1044,7 +1046,14 @@ int bs_step(const BsModelTables* T, const BsEnvState* S, const BsStepOutputs* O,
   if (!O->reward || !O->terminated || !O->truncated || !O->success || !O->fail || !O->unsupported_pairs)
     return BS_ERR_ARGUMENT;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (T->D_max <= CfgSmall::MD && T->A_max <= CfgSmall::MA) return launch<CfgSmall>(*T, *S, *O, *P, action, st);
+  static const int lanes = [] {
+    const char* v = getenv("BS_STEP_LANES");  // lanes per env for the small config (8 or 16)
+    return v ? atoi(v) : 8;
+  }();
+  if (T->D_max <= CfgSmall::MD && T->A_max <= CfgSmall::MA) {
+    if (lanes == 16) return launch<CfgSmall16>(*T, *S, *O, *P, action, st);
+    return launch<CfgSmall>(*T, *S, *O, *P, action, st);
+  }
   if (T->D_max <= CfgArt::MD && T->A_max <= CfgArt::MA) return launch<CfgArt>(*T, *S, *O, *P, action, st);
   if (T->D_max <= CfgLarge::MD && T->A_max <= CfgLarge::MA) return launch<CfgLarge>(*T, *S, *O, *P, action, st);
   return BS_ERR_UNSUPPORTED;
