@@ -486,11 +486,15 @@ def main(argv=None):
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline legs")
+    ap.add_argument("--envs", type=int, default=0, help="override envs per GPU (experiments only)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
     if args.secondary == args.config:
         args.secondary = ""
+    if args.envs:
+        WORKLOADS[args.config] = dict(WORKLOADS[args.config], envs=args.envs,
+                                      desc=WORKLOADS[args.config]["desc"] + f" [override: {args.envs} envs/GPU]")
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -8,7 +8,9 @@ timeout 600 python bench.py --steps 200 --warmup 10 > gpurun_out/${TAG}_bench.js
 if [ "$2" != "skip-ref" ]; then
   timeout 300 python bench.py --steps 50 --warmup 5 --impl reference > gpurun_out/${TAG}_bench_ref.json 2>> gpurun_out/${TAG}_bench.err
 fi
-BS_STEP_LANES=16 timeout 300 python bench.py --steps 100 --warmup 5 --no-cpu --secondary "" > gpurun_out/${TAG}_bench_c2_g16.json 2>> gpurun_out/${TAG}_bench.err
+for n in 1024 2048 8192; do
+  timeout 300 python bench.py --steps 50 --warmup 5 --no-cpu --secondary "" --envs $n > gpurun_out/${TAG}_bench_c2_n$n.json 2>> gpurun_out/${TAG}_bench.err
+done
 BS_RENDER_TILE=64 timeout 300 python bench.py --config c3 --steps 30 --warmup 3 --no-cpu --secondary "" > gpurun_out/${TAG}_bench_c3_t64.json 2>> gpurun_out/${TAG}_bench.err
 for c in c4 c5; do
   timeout 300 python bench.py --config $c --steps 30 --warmup 3 --no-cpu --secondary "" > gpurun_out/${TAG}_bench_$c.json 2>> gpurun_out/${TAG}_bench.err
