@@ -205,6 +205,11 @@ typedef struct BsSimParams {
 int bs_step(const BsModelTables* tables, const BsEnvState* state, const BsStepOutputs* out,
             const BsSimParams* params, const float* action, void* stream);
 
+/* Developer instrumentation: per-phase clock64() totals of thread 0 / CTA 0 of k_step (the
+ * per-env critical path), available when the library is built with -DBS_PHASE_TIMING
+ * (tools/phase_timing.py); BS_ERR_UNSUPPORTED otherwise.  out: host array of n <= 32. */
+int bs_debug_phase_clocks(unsigned long long* out, int32_t n, int32_t reset);
+
 /* Reset the envs selected by env_mask ([N] uint8, NULL = all) from their Philox streams,
  * then refresh the FK cache and the state obs.  Replaces env.reset. */
 int bs_reset(const BsModelTables* tables, const BsEnvState* state, const BsStepOutputs* out,

@@ -27,6 +27,8 @@ LIB_PATH = os.path.join(OUT_DIR, LIB_NAME)
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC",
           "-I" + os.path.join(ROOT, "include")]
+if os.environ.get("BS_PHASE_TIMING"):  # developer instrumentation build (tools/phase_timing.py)
+    COMMON.append("-DBS_PHASE_TIMING")
 # Per-file extra flags.  NOFMA: numpy-order arithmetic must not be contracted.
 NOFMA = ["-fmad=false"]
 SOURCES = {

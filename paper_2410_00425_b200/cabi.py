@@ -67,6 +67,7 @@ class BsFrameBatch(ctypes.Structure):
 
 _R = ctypes.POINTER
 _native.register("bs_step", [_R(BsModelTables), _R(BsEnvState), _R(BsStepOutputs), _R(BsSimParams), P, P])
+_native.register("bs_debug_phase_clocks", [P, I32, I32])
 _native.register("bs_reset", [_R(BsModelTables), _R(BsEnvState), _R(BsStepOutputs), _R(BsSimParams), P, I32, P])
 _native.register("bs_forward_kinematics", [_R(BsModelTables), _R(BsEnvState), P])
 _native.register("bs_random_actions", [ctypes.c_uint64, I64, I64, I32, I32, P, P])

@@ -31,6 +31,24 @@ using namespace bs::sim;
 
 #define FULLMASK 0xffffffffu
 
+// Phase-latency instrumentation (build with -DBS_PHASE_TIMING; tools/phase_timing.py): thread 0
+// of CTA 0 accumulates clock64() deltas per phase, so the per-env critical path can be split
+// into its phases.  Compiled out of the product build.
+#ifdef BS_PHASE_TIMING
+__device__ unsigned long long g_bs_phase[32];
+__device__ long long g_bs_last;
+#define BS_TICK(id)                                                    \
+  do {                                                                 \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                         \
+      const long long t_ = clock64();                                  \
+      g_bs_phase[id] += (unsigned long long)(t_ - g_bs_last);          \
+      g_bs_last = t_;                                                  \
+    }                                                                  \
+  } while (0)
+#else
+#define BS_TICK(id) do { } while (0)
+#endif
+
 // Per-env shared-memory layout, offsets in doubles (computed on the host from the table
 // maxima; identical for every env of the launch).
 struct Lay {
@@ -384,8 +402,10 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
   R* F = E + Y.F;
 
   fk_group<G>(M, Y, E, l);
+  BS_TICK(2);
 
-  // ---- A: per-link motion subspace + world inertia, per-shape world pose, per-actor free
+  // ---- A:
+   per-link motion subspace + world inertia, per-shape world pose, per-actor free
   //         motion (gyroscopic + gravity), zero the mass matrix
   const V3<R> grav = v3(P.gravity[0], P.gravity[1], P.gravity[2]);
   #pragma unroll 1
@@ -432,6 +452,7 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
     }
   }
   __syncwarp();
+  BS_TICK(3);
 
   // ---- B: RNEA forward pass (serial over the topological order)
   if (l == 0) {
@@ -452,6 +473,7 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
     }
   }
   __syncwarp();
+  BS_TICK(4);
   // ---- C: link forces F = I a + V x* I V (parallel over links)
   #pragma unroll 1
   for (int k = l; k < L; k += G) {
@@ -460,6 +482,7 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
     st6(F + 6 * k, add6(imul(I, ld6(Ac + 6 * k)), crossf(Vk, imul(I, Vk))));
   }
   __syncwarp();
+  BS_TICK(5);
   // ---- D: backward pass: bias forces C(q, qd) and composite inertias
   if (l == 0) {
     for (int k = L - 1; k >= 0; --k) {
@@ -476,6 +499,7 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
     }
   }
   __syncwarp();
+  BS_TICK(6);
   // ---- E: CRBA mass matrix (parallel over dof links)
   #pragma unroll 1
   for (int k = l; k < L; k += G) {
@@ -491,6 +515,7 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
     }
   }
   __syncwarp();
+  BS_TICK(7);
   // ---- F: implicit PD drives (A-16) and Cholesky of Mt (lane 0; inverse diagonal kept)
   if (l == 0) {
     for (int i = 0; i < D; ++i) {
@@ -514,6 +539,7 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
     }
   }
   __syncwarp();
+  BS_TICK(8);
   // ---- G: columns of M^-1 (lanes j < D) and the unconstrained velocity (lane D)
   #pragma unroll 1
   for (int j = l; j <= D; j += G) {
@@ -549,6 +575,7 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
         if (i < D) E[Y.u + i] = E[Y.qd + i] + dt * x[i];
     }
   }
+  BS_TICK(9);
   // ---- H: broadphase + narrowphase into fixed per-pair candidate slots (A-5)
   R* cand = E + Y.rows;  // candidates alias the (not yet built) row storage
   const R slop = P.slop;
@@ -564,6 +591,7 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
   for (int o = G / 2; o > 0; o >>= 1) unsup += __shfl_xor_sync(FULLMASK, unsup, o);
   unsupported = unsup;
   __syncwarp();
+  BS_TICK(10);
   // ---- I: ordered compaction of the valid slots (ballot + popc within the group)
   R* ct = E + Y.ct;
   {
@@ -583,6 +611,7 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
     nc = base;
   }
   __syncwarp();
+  BS_TICK(11);
   // ---- J: constraint rows (normal, t1, t2 per contact; parallel over rows)
   R* rows = E + Y.rows;
   const int RW = Y.RW, NU = Y.NU;
@@ -645,47 +674,69 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
     row[3] = depth < 0.0 ? depth / dt : 0.0;
   }
   __syncwarp();
+  BS_TICK(12);
 
   // ---- K: projected Gauss-Seidel, sequential row order.  The velocity
-  //         vector is distributed over the group (lane l owns u[l], u[l+G], ...): each row is a
-  //         lane-local partial dot, a 3-level shuffle all-reduce inside the group, the
-  //         (redundant) multiplier update, and a lane-local axpy.
-  constexpr int NUM = K::NU, KU = (NUM + G - 1) / G;
+  //         vector lives on PL lanes of the group (lane l < PL owns u[l], u[l+PL], ...): each row
+  //         is a lane-local partial dot, a log2(PL)-level shuffle all-reduce, the multiplier
+  //         update and a lane-local axpy.  The next row's data is prefetched into registers
+  //         while the current row's dependency chain runs (the sweep is latency-bound).
+  constexpr int NUM = K::NU, PL = NUM <= 10 ? 2 : (NUM <= 20 ? 4 : 8), KP = (NUM + PL - 1) / PL;
   const unsigned gmask = (G == 32 ? FULLMASK : ((1u << G) - 1u)) << (g * G);
-  R u[KU];
+  const bool owner = l < PL;
+  R u[KP];
 #pragma unroll
-  for (int j = 0; j < KU; ++j) {
-    const int k = l + G * j;
-    u[j] = k < NU ? E[Y.u + k] : 0.0;
+  for (int j = 0; j < KP; ++j) {
+    const int k = l + PL * j;
+    u[j] = owner && k < NU ? E[Y.u + k] : 0.0;
   }
   const int iters = P.pos_iters + P.vel_iters;
+  const int nrows = 3 * nc;
   const R mu = P.friction;
   for (int it = 0; it < iters; ++it) {
     const bool pos_phase = it < P.pos_iters;
-    R* row = rows;
-    for (int c = 0; c < nc; ++c) {
-      R lam_n = 0.0;
+    // prefetch row 0
+    R n_invK = 0.0, n_old = 0.0, n_tgt = 0.0, n_J[KP], n_W[KP];
 #pragma unroll
-      for (int rr = 0; rr < 3; ++rr, row += RW) {
-        const R invK = row[0];
-        const R old = row[1];
-        if (invK == 0.0) {
-          if (rr == 0) lam_n = old;
-          continue;
+    for (int j = 0; j < KP; ++j) { n_J[j] = 0.0; n_W[j] = 0.0; }
+    if (nrows) {
+      const R* rw = rows;
+      n_invK = rw[0]; n_old = rw[1]; n_tgt = pos_phase ? rw[2] : rw[3];
+#pragma unroll
+      for (int j = 0; j < KP; ++j) {
+        const int k = l + PL * j;
+        if (owner && k < NU) { n_J[j] = rw[ROW_J + k]; n_W[j] = rw[ROW_J + NU + k]; }
+      }
+    }
+    R lam_n = 0.0;
+    int rr = 0;
+    for (int r = 0; r < nrows; ++r) {
+      const R invK = n_invK, old = n_old, tgt = n_tgt;
+      R Jc[KP], Wc[KP];
+#pragma unroll
+      for (int j = 0; j < KP; ++j) { Jc[j] = n_J[j]; Wc[j] = n_W[j]; }
+      R* row = rows + r * RW;
+      if (r + 1 < nrows) {  // prefetch the next row
+        const R* rw = row + RW;
+        n_invK = rw[0]; n_old = rw[1]; n_tgt = pos_phase ? rw[2] : rw[3];
+#pragma unroll
+        for (int j = 0; j < KP; ++j) {
+          const int k = l + PL * j;
+          if (owner && k < NU) { n_J[j] = rw[ROW_J + k]; n_W[j] = rw[ROW_J + NU + k]; }
         }
-        const R* J = row + ROW_J;
-        const R* Wr = J + NU;
-        R v = 0.0;
+      }
+      if (invK != 0.0) {
+        R v0 = 0.0, v1 = 0.0;
 #pragma unroll
-        for (int j = 0; j < KU; ++j) {
-          const int k = l + G * j;
-          if (k < NU) v += J[k] * u[j];
+        for (int j = 0; j < KP; j += 2) {
+          v0 += Jc[j] * u[j];
+          if (j + 1 < KP) v1 += Jc[j + 1] * u[j + 1];
         }
+        R v = v0 + v1;
 #pragma unroll
-        for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(gmask, v, o);
+        for (int o = PL / 2; o > 0; o >>= 1) v += __shfl_xor_sync(gmask, v, o);
         R nw;
         if (rr == 0) {
-          const R tgt = pos_phase ? row[2] : row[3];
           nw = fmax(old + (tgt - v) * invK, 0.0);
           lam_n = nw;
         } else {
@@ -693,21 +744,22 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
           nw = fmin(fmax(old + (0.0 - v) * invK, -bound), bound);
         }
         const R delta = nw - old;
-        row[1] = nw;  // every lane stores the same value and reads back its own
+        if (owner) row[1] = nw;  // owner lanes store the same value and read back their own
 #pragma unroll
-        for (int j = 0; j < KU; ++j) {
-          const int k = l + G * j;
-          if (k < NU) u[j] += delta * Wr[k];
-        }
+        for (int j = 0; j < KP; ++j) u[j] += delta * Wc[j];
+      } else if (rr == 0) {
+        lam_n = old;
       }
+      rr = rr == 2 ? 0 : rr + 1;
     }
   }
 #pragma unroll
-  for (int j = 0; j < KU; ++j) {
-    const int k = l + G * j;
-    if (k < NU) E[Y.u + k] = u[j];
+  for (int j = 0; j < KP; ++j) {
+    const int k = l + PL * j;
+    if (owner && k < NU) E[Y.u + k] = u[j];
   }
   __syncwarp();
+  BS_TICK(13);
 
   // ---- L: semi-implicit Euler, joint limits (A-7), actor orientation (A-8), divergence
   //         freeze.  Every lane evaluates the (small) update from the
@@ -765,6 +817,7 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
       }
   }
   __syncwarp();
+  BS_TICK(14);
 }
 
 // ------------------------------------------------------------------ the kernel
@@ -781,6 +834,7 @@ __global__ void __launch_bounds__(32) k_step(BsModelTables T, BsEnvState S, BsSt
   R* E = smem + g * Y.total;
   const Model M = model_of(T, S.model_id[e]);
   const int Dm = Y.Dm, Am = Y.Am;
+  BS_TICK(0);
 
   // ---- stage the env's state rows
   #pragma unroll 1
@@ -843,6 +897,7 @@ __global__ void __launch_bounds__(32) k_step(BsModelTables T, BsEnvState S, BsSt
   }
   bool diverged = S.diverged[e] != 0;
   __syncwarp();
+  BS_TICK(1);
 
   int unsupported = 0, nc = 0;
   for (int s = 0; s < P.substeps; ++s) {
@@ -863,6 +918,7 @@ __global__ void __launch_bounds__(32) k_step(BsModelTables T, BsEnvState S, BsSt
     }
   }
   fk_group<G>(M, Y, E, l);
+  BS_TICK(15);
 
   // ---- task evaluation; every lane evaluates (cheap, uniform)
   const R* lpq = E + Y.lpq;
@@ -936,6 +992,7 @@ __global__ void __launch_bounds__(32) k_step(BsModelTables T, BsEnvState S, BsSt
     __syncwarp();
     fk_group<G>(M, Y, E, l);
   }
+  BS_TICK(16);
   if (!live) return;
   // ---- write back the state rows, the FK cache and the state observation
   #pragma unroll 1
@@ -973,6 +1030,7 @@ __global__ void __launch_bounds__(32) k_step(BsModelTables T, BsEnvState S, BsSt
       o[k] = (float)v;
     }
   }
+  BS_TICK(17);
 }
 
 // ------------------------------------------------------------------ host side
@@ -1038,6 +1096,21 @@ typedef Cfg<8, 12, 4> CfgLarge;   // general scenes: D <= 12, <= 4 actors
 using namespace bs::step;
 
 extern "C" {
+
+int bs_debug_phase_clocks(unsigned long long* out, int32_t n, int32_t reset) {
+#ifdef BS_PHASE_TIMING
+  if (!out || n < 0 || n > 32) return BS_ERR_ARGUMENT;
+  if (cudaMemcpyFromSymbol(out, g_bs_phase, sizeof(unsigned long long) * n) != cudaSuccess) return BS_ERR_CUDA;
+  if (reset) {
+    unsigned long long z[32] = {0};
+    if (cudaMemcpyToSymbol(g_bs_phase, z, sizeof(z)) != cudaSuccess) return BS_ERR_CUDA;
+  }
+  return BS_OK;
+#else
+  (void)out; (void)n; (void)reset;
+  return BS_ERR_UNSUPPORTED;
+#endif
+}
 
 int bs_step(const BsModelTables* T, const BsEnvState* S, const BsStepOutputs* O, const BsSimParams* P,
             const float* action, void* stream) {
