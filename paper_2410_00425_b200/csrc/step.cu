@@ -404,8 +404,7 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
   fk_group<G>(M, Y, E, l);
   BS_TICK(2);
 
-  // ---- A:
-   per-link motion subspace + world inertia, per-shape world pose, per-actor free
+  // ---- A: per-link motion subspace + world inertia, per-shape world pose, per-actor free
   //         motion (gyroscopic + gravity), zero the mass matrix
   const V3<R> grav = v3(P.gravity[0], P.gravity[1], P.gravity[2]);
   #pragma unroll 1
