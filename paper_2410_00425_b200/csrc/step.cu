@@ -45,8 +45,13 @@ __device__ long long g_bs_last;
       g_bs_last = t_;                                                  \
     }                                                                  \
   } while (0)
+#define BS_COUNT(id, v)                                                        \
+  do {                                                                         \
+    if (blockIdx.x == 0 && threadIdx.x == 0) g_bs_phase[id] += (unsigned long long)(v); \
+  } while (0)
 #else
 #define BS_TICK(id) do { } while (0)
+#define BS_COUNT(id, v) do { } while (0)
 #endif
 
 // Per-env shared-memory layout, offsets in doubles (computed on the host from the table
@@ -67,9 +72,12 @@ struct Lay {
 // no actor-index selects and no int conversions in the sweep.
 #define ROW_J 4
 
-template <int G_, int MD_, int MA_>
+// EX_ = the launch guarantees D_max == MD and A_max == MA exactly, so the padded widths
+// (D_max, A_max, NU and the row stride) are compile-time constants in the kernel.
+template <int G_, int MD_, int MA_, bool EX_ = false>
 struct Cfg {
   static constexpr int G = G_, MD = MD_, MA = MA_, EPW = 32 / G_, NU = MD_ + 6 * MA_;
+  static constexpr bool EXACT = EX_;
 };
 
 __device__ __forceinline__ R sgn_of(R v) { return v > 0.0 ? 1.0 : -1.0; }
@@ -389,7 +397,7 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
                         bool& diverged, int& unsupported, int& nc) {
   constexpr int G = K::G, MD = K::MD, MA = K::MA;
   const R dt = P.dt;
-  const int L = M.L, D = M.D, A = M.A, NS = M.S, Dm = Y.Dm;
+  const int L = M.L, D = M.D, A = M.A, NS = M.S, Dm = K::EXACT ? MD : Y.Dm;
   R* lpq = E + Y.lpq;
   R* Sv = E + Y.Sv;
   R* In = E + Y.In;
@@ -613,7 +621,7 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
   BS_TICK(11);
   // ---- J: constraint rows (normal, t1, t2 per contact; parallel over rows)
   R* rows = E + Y.rows;
-  const int RW = Y.RW, NU = Y.NU;
+  const int NU = K::EXACT ? K::NU : Y.NU, RW = ROW_J + 2 * NU;
   #pragma unroll 1
   for (int r = l; r < 3 * nc; r += G) {
     const int c = r / 3, rr = r - 3 * c;
@@ -675,48 +683,104 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
   __syncwarp();
   BS_TICK(12);
 
-  // ---- K: projected Gauss-Seidel, sequential row order.  The velocity
-  //         vector lives on PL lanes of the group (lane l < PL owns u[l], u[l+PL], ...): each row
-  //         is a lane-local partial dot, a log2(PL)-level shuffle all-reduce, the multiplier
-  //         update and a lane-local axpy.  The next row's data is prefetched into registers
-  //         while the current row's dependency chain runs (the sweep is latency-bound).
-  constexpr int NUM = K::NU, PL = NUM <= 10 ? 2 : (NUM <= 20 ? 4 : 8), KP = (NUM + PL - 1) / PL;
-  const unsigned gmask = (G == 32 ? FULLMASK : ((1u << G) - 1u)) << (g * G);
-  const bool owner = l < PL;
-  R u[KP];
-#pragma unroll
-  for (int j = 0; j < KP; ++j) {
-    const int k = l + PL * j;
-    u[j] = owner && k < NU ? E[Y.u + k] : 0.0;
-  }
+  // ---- K: projected Gauss-Seidel, sequential row order.
+  constexpr int NUM = K::NU;
   const int iters = P.pos_iters + P.vel_iters;
   const int nrows = 3 * nc;
   const R mu = P.friction;
-  for (int it = 0; it < iters; ++it) {
-    const bool pos_phase = it < P.pos_iters;
-    // prefetch row 0
-    R n_invK = 0.0, n_old = 0.0, n_tgt = 0.0, n_J[KP], n_W[KP];
+  if constexpr (NUM <= 12) {
+    // Small u (PickCube-style scenes): every lane of the group holds all of u in registers and
+    // evaluates each row redundantly, so a row is a register dot product, the multiplier
+    // update and a register axpy -- no shuffles on the dependency chain.  The sweep walks one
+    // contact (normal, t1, t2) per iteration with the friction bound in a register; the
+    // multipliers are stored after the three rows, so the loads of all three rows can issue
+    // ahead of the first row's chain.  The warp's groups sweep in lockstep to the largest
+    // contact count of the warp (rows past an env's own count are predicated off; their W was
+    // zeroed here), so the sweep has no divergent control flow.
+    int ncw = nc;
 #pragma unroll
-    for (int j = 0; j < KP; ++j) { n_J[j] = 0.0; n_W[j] = 0.0; }
-    if (nrows) {
-      const R* rw = rows;
-      n_invK = rw[0]; n_old = rw[1]; n_tgt = pos_phase ? rw[2] : rw[3];
+    for (int o = G; o < 32; o <<= 1) ncw = max(ncw, __shfl_xor_sync(FULLMASK, ncw, o));
+    BS_COUNT(20, nc);
+    BS_COUNT(21, ncw);
+    #pragma unroll 1
+    for (int r = nrows; r < 3 * ncw; ++r)
+      for (int k = l; k < NU; k += G) rows[r * RW + ROW_J + NU + k] = 0.0;
+    __syncwarp();
+    R u[NUM];
 #pragma unroll
-      for (int j = 0; j < KP; ++j) {
-        const int k = l + PL * j;
-        if (owner && k < NU) { n_J[j] = rw[ROW_J + k]; n_W[j] = rw[ROW_J + NU + k]; }
+    for (int j = 0; j < NUM; ++j) u[j] = j < NU ? E[Y.u + j] : 0.0;
+    for (int it = 0; it < iters; ++it) {
+      const int tsel = it < P.pos_iters ? 2 : 3;  // position- or velocity-phase target
+      #pragma unroll 1
+      for (int c = 0; c < ncw; ++c) {
+        R* r0 = rows + 3 * c * RW;
+        const bool live = c < nc;
+        R Jc[3][NUM], Wc[3][NUM], invK[3], old[3], nw[3];
+        bool act[3];
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+          const R* rt = r0 + t * RW;
+          invK[t] = rt[0];
+          old[t] = rt[1];
+          act[t] = live && invK[t] != 0.0;
+#pragma unroll
+          for (int j = 0; j < NUM; ++j) {
+            Jc[t][j] = j < NU ? rt[ROW_J + j] : 0.0;
+            Wc[t][j] = j < NU ? rt[ROW_J + NU + j] : 0.0;
+          }
+        }
+        const R tgt = r0[tsel];
+        R bound = 0.0;
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+          R a0 = 0.0, a1 = 0.0, a2 = 0.0;
+#pragma unroll
+          for (int j = 0; j < NUM; j += 3) {
+            a0 = fma(Jc[t][j], u[j], a0);
+            if (j + 1 < NUM) a1 = fma(Jc[t][j + 1], u[j + 1], a1);
+            if (j + 2 < NUM) a2 = fma(Jc[t][j + 2], u[j + 2], a2);
+          }
+          const R v = (a0 + a1) + a2;
+          if (t == 0) {
+            const R x = old[0] + (tgt - v) * invK[0];
+            nw[0] = x > 0.0 ? x : 0.0;
+            bound = mu * (act[0] ? nw[0] : old[0]);
+          } else {
+            const R x = old[t] - v * invK[t];
+            nw[t] = x < -bound ? -bound : (x > bound ? bound : x);
+          }
+          const R delta = act[t] ? nw[t] - old[t] : 0.0;
+#pragma unroll
+          for (int j = 0; j < NUM; ++j) u[j] = fma(delta, Wc[t][j], u[j]);
+        }
+#pragma unroll
+        for (int t = 0; t < 3; ++t)
+          if (act[t]) r0[t * RW + 1] = nw[t];  // every lane stores the same value
       }
     }
-    R lam_n = 0.0;
-    int rr = 0;
-    for (int r = 0; r < nrows; ++r) {
-      const R invK = n_invK, old = n_old, tgt = n_tgt;
-      R Jc[KP], Wc[KP];
 #pragma unroll
-      for (int j = 0; j < KP; ++j) { Jc[j] = n_J[j]; Wc[j] = n_W[j]; }
-      R* row = rows + r * RW;
-      if (r + 1 < nrows) {  // prefetch the next row
-        const R* rw = row + RW;
+    for (int j = 0; j < NUM; ++j)
+      if (l == 0 && j < NU) E[Y.u + j] = u[j];
+  } else {
+    // Larger u: the velocity vector lives on PL lanes of the group (lane l < PL owns u[l],
+    // u[l+PL], ...); each row is a lane-local partial dot, a log2(PL)-level shuffle all-reduce,
+    // the multiplier update and a lane-local axpy.
+    constexpr int PL = NUM <= 20 ? 4 : 8, KP = (NUM + PL - 1) / PL;
+    const unsigned gmask = (G == 32 ? FULLMASK : ((1u << G) - 1u)) << (g * G);
+    const bool owner = l < PL;
+    R u[KP];
+#pragma unroll
+    for (int j = 0; j < KP; ++j) {
+      const int k = l + PL * j;
+      u[j] = owner && k < NU ? E[Y.u + k] : 0.0;
+    }
+    for (int it = 0; it < iters; ++it) {
+      const bool pos_phase = it < P.pos_iters;
+      R n_invK = 0.0, n_old = 0.0, n_tgt = 0.0, n_J[KP], n_W[KP];
+#pragma unroll
+      for (int j = 0; j < KP; ++j) { n_J[j] = 0.0; n_W[j] = 0.0; }
+      if (nrows) {
+        const R* rw = rows;
         n_invK = rw[0]; n_old = rw[1]; n_tgt = pos_phase ? rw[2] : rw[3];
 #pragma unroll
         for (int j = 0; j < KP; ++j) {
@@ -724,38 +788,56 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
           if (owner && k < NU) { n_J[j] = rw[ROW_J + k]; n_W[j] = rw[ROW_J + NU + k]; }
         }
       }
-      if (invK != 0.0) {
-        R v0 = 0.0, v1 = 0.0;
+      R lam_n = 0.0;
+      int rr = 0;
+      for (int r = 0; r < nrows; ++r) {
+        const R invK = n_invK, old = n_old, tgt = n_tgt;
+        R Jc[KP], Wc[KP];
 #pragma unroll
-        for (int j = 0; j < KP; j += 2) {
-          v0 += Jc[j] * u[j];
-          if (j + 1 < KP) v1 += Jc[j + 1] * u[j + 1];
+        for (int j = 0; j < KP; ++j) { Jc[j] = n_J[j]; Wc[j] = n_W[j]; }
+        R* row = rows + r * RW;
+        if (r + 1 < nrows) {  // prefetch the next row
+          const R* rw = row + RW;
+          n_invK = rw[0]; n_old = rw[1]; n_tgt = pos_phase ? rw[2] : rw[3];
+#pragma unroll
+          for (int j = 0; j < KP; ++j) {
+            const int k = l + PL * j;
+            if (owner && k < NU) { n_J[j] = rw[ROW_J + k]; n_W[j] = rw[ROW_J + NU + k]; }
+          }
         }
-        R v = v0 + v1;
+        if (invK != 0.0) {
+          R v0 = 0.0, v1 = 0.0;
 #pragma unroll
-        for (int o = PL / 2; o > 0; o >>= 1) v += __shfl_xor_sync(gmask, v, o);
-        R nw;
-        if (rr == 0) {
-          nw = fmax(old + (tgt - v) * invK, 0.0);
-          lam_n = nw;
-        } else {
-          const R bound = mu * lam_n;
-          nw = fmin(fmax(old + (0.0 - v) * invK, -bound), bound);
+          for (int j = 0; j < KP; j += 2) {
+            v0 += Jc[j] * u[j];
+            if (j + 1 < KP) v1 += Jc[j + 1] * u[j + 1];
+          }
+          R v = v0 + v1;
+#pragma unroll
+          for (int o = PL / 2; o > 0; o >>= 1) v += __shfl_xor_sync(gmask, v, o);
+          R nw;
+          if (rr == 0) {
+            nw = fmax(old + (tgt - v) * invK, 0.0);
+            lam_n = nw;
+          } else {
+            const R bound = mu * lam_n;
+            nw = fmin(fmax(old + (0.0 - v) * invK, -bound), bound);
+          }
+          const R delta = nw - old;
+          if (owner) row[1] = nw;  // owner lanes store the same value and read back their own
+#pragma unroll
+          for (int j = 0; j < KP; ++j) u[j] += delta * Wc[j];
+        } else if (rr == 0) {
+          lam_n = old;
         }
-        const R delta = nw - old;
-        if (owner) row[1] = nw;  // owner lanes store the same value and read back their own
-#pragma unroll
-        for (int j = 0; j < KP; ++j) u[j] += delta * Wc[j];
-      } else if (rr == 0) {
-        lam_n = old;
+        rr = rr == 2 ? 0 : rr + 1;
       }
-      rr = rr == 2 ? 0 : rr + 1;
     }
-  }
 #pragma unroll
-  for (int j = 0; j < KP; ++j) {
-    const int k = l + PL * j;
-    if (owner && k < NU) E[Y.u + k] = u[j];
+    for (int j = 0; j < KP; ++j) {
+      const int k = l + PL * j;
+      if (owner && k < NU) E[Y.u + k] = u[j];
+    }
   }
   __syncwarp();
   BS_TICK(13);
@@ -832,7 +914,7 @@ __global__ void __launch_bounds__(32) k_step(BsModelTables T, BsEnvState S, BsSt
   const int e = live ? e_raw : S.num_envs - 1;  // idle groups shadow the last env, never store
   R* E = smem + g * Y.total;
   const Model M = model_of(T, S.model_id[e]);
-  const int Dm = Y.Dm, Am = Y.Am;
+  const int Dm = K::EXACT ? MD : Y.Dm, Am = K::EXACT ? MA : Y.Am;
   BS_TICK(0);
 
   // ---- stage the env's state rows
@@ -1084,8 +1166,8 @@ static int launch(const BsModelTables& T, const BsEnvState& S, const BsStepOutpu
   return launch_status();
 }
 
+typedef Cfg<8, 3, 1, true> CfgPick;  // exactly ARM3 + one free actor (PickCube, PickHetero): static widths
 typedef Cfg<8, 4, 1> CfgSmall;    // PickCube-style: D <= 4, one free actor
-typedef Cfg<16, 4, 1> CfgSmall16; // same with 16 lanes per env (2 envs per warp), BS_STEP_LANES=16
 typedef Cfg<8, 12, 1> CfgArt;     // articulated objects (arm + cabinet): D <= 12, <= 1 actor
 typedef Cfg<8, 12, 4> CfgLarge;   // general scenes: D <= 12, <= 4 actors
 
@@ -1118,14 +1200,12 @@ int bs_step(const BsModelTables* T, const BsEnvState* S, const BsStepOutputs* O,
   if (!O->reward || !O->terminated || !O->truncated || !O->success || !O->fail || !O->unsupported_pairs)
     return BS_ERR_ARGUMENT;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  static const int lanes = [] {
-    const char* v = getenv("BS_STEP_LANES");  // lanes per env for the small config (8 or 16)
-    return v ? atoi(v) : 8;
+  static const bool generic = [] {
+    const char* v = getenv("BS_STEP_GENERIC");  // tests: force the runtime-width variants
+    return v && atoi(v) != 0;
   }();
-  if (T->D_max <= CfgSmall::MD && T->A_max <= CfgSmall::MA) {
-    if (lanes == 16) return launch<CfgSmall16>(*T, *S, *O, *P, action, st);
-    return launch<CfgSmall>(*T, *S, *O, *P, action, st);
-  }
+  if (!generic && T->D_max == CfgPick::MD && T->A_max == CfgPick::MA) return launch<CfgPick>(*T, *S, *O, *P, action, st);
+  if (T->D_max <= CfgSmall::MD && T->A_max <= CfgSmall::MA) return launch<CfgSmall>(*T, *S, *O, *P, action, st);
   if (T->D_max <= CfgArt::MD && T->A_max <= CfgArt::MA) return launch<CfgArt>(*T, *S, *O, *P, action, st);
   if (T->D_max <= CfgLarge::MD && T->A_max <= CfgLarge::MA) return launch<CfgLarge>(*T, *S, *O, *P, action, st);
   return BS_ERR_UNSUPPORTED;

@@ -330,3 +330,19 @@ def test_base_forward_rotate_matches_oracle(cuda):
         assert np.abs(env.scene.qpos.cpu().numpy() - st.q).max() < 1e-9, t
     q = env.scene.qpos.cpu().numpy()
     assert (np.hypot(q[:, 0], q[:, 1]) > 0.005).all()  # moved forward along the heading
+
+
+def test_generic_width_kernel_variant(cuda):
+    """The PickCube scene normally runs the static-width kernel variant (D_max == 3, A_max == 1);
+    rerun the parity tests of this module on the runtime-width variant (BS_STEP_GENERIC=1)."""
+    import os
+    import subprocess
+    import sys
+
+    if os.environ.get("BS_STEP_GENERIC"):
+        pytest.skip("already running the generic variant")
+    env = dict(os.environ, BS_STEP_GENERIC="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", __file__, "-k",
+                        "one_step_parity or trajectory_parity or ee_delta or episode_metrics"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]

@@ -20,4 +20,7 @@ BENCH_DIST_BACKEND=gloo timeout 300 python -m torch.distributed.run --nnodes=1 -
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 5 --warmup 3 --no-cpu > /dev/null 2>> gpurun_out/${TAG}_ncu.err
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_step -s 3 -c 1 -o gpurun_out/${TAG}_prof_step python bench.py --steps 3 --warmup 3 --no-cpu --secondary "" > /dev/null 2>> gpurun_out/${TAG}_ncu.err
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_render -s 3 -c 1 -o gpurun_out/${TAG}_prof_render python bench.py --config c3 --steps 3 --warmup 3 --no-cpu --secondary "" > /dev/null 2>> gpurun_out/${TAG}_ncu.err
+if [ "$3" == "phase" ]; then
+  timeout 600 python tools/phase_timing.py 4096 50 > gpurun_out/${TAG}_phase.txt 2>&1
+fi
 echo done

@@ -57,6 +57,10 @@ def main():
     for i, v in sorted(vals.items(), key=lambda x: -x[1]):
         print(f"{v:10.0f} cyc  {100 * v / tot:5.1f}%  {NAMES.get(i, i)}")
     print(f"total {tot:.0f} cycles per step ({tot / 1.965e3:.1f} us at 1965 MHz)")
+    subs = 2 * steps  # substeps per step (PickCube: sim 120 Hz / control 60 Hz)
+    out["contacts_env0_per_substep"] = buf[20] / subs
+    out["contacts_warp_max_per_substep"] = buf[21] / subs
+    print(f"contacts per substep: env0 {buf[20] / subs:.2f}, warp max {buf[21] / subs:.2f}")
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", "phase_timing.json"), "w") as f:
         json.dump(out, f, indent=1)
