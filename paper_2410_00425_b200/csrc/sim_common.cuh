@@ -232,7 +232,7 @@ __device__ __forceinline__ Q4<R> qnorm_rn(Q4<R> q) {
   return Q4<R>{__dmul_rn(r.w, s), __dmul_rn(r.x, s), __dmul_rn(r.y, s), __dmul_rn(r.z, s)};
 }
 
-static __device__ __noinline__ void task_reset(const Model& M, const BsSimParams& P, int64_t genv, uint32_t rc, R* q, R* qd,
+static __device__ __noinline__ void task_reset(const Model M, const BsSimParams& P, int64_t genv, uint32_t rc, R* q, R* qd,
                            V3<R>* ap, Q4<R>* aq, V3<R>* av, V3<R>* aw, R* goal, int32_t* target_dof) {
   uint32_t k0 = (uint32_t)(P.seed & 0xffffffffu), k1 = (uint32_t)(P.seed >> 32);
   R u[8];
@@ -274,7 +274,7 @@ __device__ __forceinline__ R dist3(V3<R> a, V3<R> b) {
   return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
 }
 
-static __device__ void task_eval(const Model& M, const BsSimParams& P, const V3<R>* lp, const R* q,
+static __device__ __forceinline__ void task_eval(const Model& M, const BsSimParams& P, const V3<R>* lp, const R* q,
                           const V3<R>* ap, const R* goal, int tdof, bool diverged, float& reward,
                           bool& success, bool& fail) {
   if (P.task == BS_TASK_PICKCUBE) {
@@ -298,7 +298,7 @@ static __device__ void task_eval(const Model& M, const BsSimParams& P, const V3<
   }
 }
 
-static __device__ void pack_obs(const Model& M, const BsSimParams& P, int Dm, int Am, const R* q, const R* qd,
+static __device__ __forceinline__ void pack_obs(const Model& M, const BsSimParams& P, int Dm, int Am, const R* q, const R* qd,
                          const V3<R>* lp, const V3<R>* ap, const Q4<R>* aq, const V3<R>* av,
                          const V3<R>* aw, const R* goal, float* o, int obs_dim) {
   // layout: q[D_max] qd[D_max] ee_p[3]

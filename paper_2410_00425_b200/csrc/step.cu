@@ -170,7 +170,7 @@ __device__ __forceinline__ void put_cand(R* c, V3<R> sB, V3<R> n, R depth, int p
 
 // Narrowphase of one static pair (A-4, A-25) into its fixed slots.
 // Returns 1 when the pair passed the broadphase but has no routine (A-23).
-__device__ int narrow_pair(const Model& M, int pi, const R* spq, R slop, R* cand) {
+__device__ __forceinline__ int narrow_pair(const Model& M, int pi, const R* spq, R slop, R* cand) {
   const int i = M.p_i[pi], j = M.p_j[pi], code = M.p_code[pi];
   const int ki = M.s_kind[i], kj = M.s_kind[j];
   const int mc = pair_maxc(code);
@@ -326,7 +326,7 @@ __device__ __forceinline__ void fk_group(const Model& M, const Lay& Y, R* E, int
 }
 
 // pd_ee_delta_pose targets (lane 0 of the group; rarely on the hot path, kept out of line).
-__device__ __noinline__ void ee_delta_targets(const Model& M, const BsSimParams& P, const Lay& Y, R* E,
+__device__ __noinline__ void ee_delta_targets(const Model M, const BsSimParams& P, const Lay& Y, R* E,
                                               const float* act) {
   const int Dm = Y.Dm;
       R* Jm = E + Y.rows;        // 6 x Dm, scratch (rows are rebuilt every substep)
@@ -393,7 +393,7 @@ __device__ __noinline__ void ee_delta_targets(const Model& M, const BsSimParams&
 
 // ------------------------------------------------------------------ one substep
 template <class K>
-__device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E, const int l, const int g,
+__device__ __forceinline__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E, const int l, const int g,
                         bool& diverged, int& unsupported, int& nc) {
   constexpr int G = K::G, MD = K::MD, MA = K::MA;
   const R dt = P.dt;
@@ -903,8 +903,9 @@ __device__ void substep(const Model& M, const BsSimParams& P, const Lay& Y, R* E
 
 // ------------------------------------------------------------------ the kernel
 template <class K>
-__global__ void __launch_bounds__(32) k_step(BsModelTables T, BsEnvState S, BsStepOutputs O, BsSimParams P,
-                                             const float* __restrict__ action, Lay Y) {
+__global__ void __launch_bounds__(32) k_step(const __grid_constant__ BsModelTables T, const __grid_constant__ BsEnvState S,
+                                             const __grid_constant__ BsStepOutputs O, const __grid_constant__ BsSimParams P,
+                                             const float* __restrict__ action, const __grid_constant__ Lay Y) {
   constexpr int G = K::G, MD = K::MD, MA = K::MA, EPW = K::EPW;
   extern __shared__ double smem[];
   const int lane = threadIdx.x;
