@@ -22,6 +22,7 @@
 // step is a dense contraction, so there are no tensor cores; the kernel is latency/ALU
 // bound and moves ~0.8 KB of HBM per env-step.
 #include <stdlib.h>
+#include <string.h>
 #include "sim_common.cuh"
 
 namespace bs {
@@ -67,10 +68,14 @@ struct Lay {
 // Generalised velocity u (length NU = D_max + 6 A_max): [0, D_max) joint rates, then per actor
 // slot a: linear velocity at [D_max + 6a, +3), angular at [D_max + 6a + 3, +3).
 // Row layout (dense over u): [0] 1/K (0 = skip)  [1] lambda  [2] position-phase target
-// [3] velocity-phase target  [4, 4+NU) J  [4+NU, 4+2NU) W = M_u^-1 J^T (the velocity change per
-// unit impulse).  Rows touch at most two bodies, but a dense row has no per-row branching,
-// no actor-index selects and no int conversions in the sweep.
+// [3] velocity-phase target, then NU interleaved pairs (J[k], W[k]) at [4 + 2k, 4 + 2k + 1],
+// W = M_u^-1 J^T (the velocity change per unit impulse).  Rows start 16-byte aligned (the
+// layout keeps every offset even), so the sweep reads the scalars and each (J, W) pair with
+// one 16-byte shared load.  Rows touch at most two bodies, but a dense row has no per-row
+// branching, no actor-index selects and no int conversions in the sweep.
 #define ROW_J 4
+#define JI(k) (ROW_J + 2 * (k))
+#define WI(k) (ROW_J + 2 * (k) + 1)
 
 // EX_ = the launch guarantees D_max == MD and A_max == MA exactly, so the padded widths
 // (D_max, A_max, NU and the row stride) are compile-time constants in the kernel.
@@ -619,32 +624,30 @@ __device__ __forceinline__ void substep(const Model& M, const BsSimParams& P, co
   }
   __syncwarp();
   BS_TICK(11);
-  // ---- J: constraint rows (normal, t1, t2 per contact; parallel over rows)
+  // ---- J: constraint rows.  One lane per contact builds its normal and two tangent rows
+  //         (shared slots, lever arms and chain walk; three independent reciprocals).
   R* rows = E + Y.rows;
   const int NU = K::EXACT ? K::NU : Y.NU, RW = ROW_J + 2 * NU;
   #pragma unroll 1
-  for (int r = l; r < 3 * nc; r += G) {
-    const int c = r / 3, rr = r - 3 * c;
+  for (int c = l; c < nc; c += G) {
     const R* cc = ct + 8 * c;
     const V3<R> Pc = ld3(cc), n = ld3(cc + 3);
     const R depth = cc[6];
     const int pi = (int)cc[7];
-    V3<R> dir = n;
-    if (rr) {  // tangent basis (A-6)
+    V3<R> dirs[3];
+    {  // tangent basis (A-6): t1 = normalize(n x e_k), e_k the least-aligned axis; t2 = n x t1
       const R an[3] = {fabs(n.x), fabs(n.y), fabs(n.z)};
       int k = 0;
       if (an[1] < an[k]) k = 1;
       if (an[2] < an[k]) k = 2;
       V3<R> t1 = crs(n, v3(k == 0, k == 1, k == 2));
       t1 = scl(t1, rsqrt(dot(t1, t1)));
-      dir = rr == 1 ? t1 : crs(n, t1);
+      dirs[0] = n; dirs[1] = t1; dirs[2] = crs(n, t1);
     }
-    R* row = rows + r * RW;
-    R* J = row + ROW_J;
-    R* W = J + NU;
-    for (int k = 0; k < NU; ++k) { J[k] = 0.0; W[k] = 0.0; }
+    R* r0 = rows + 3 * c * RW;
+    for (int k = 0; k < 3 * RW; k += 2) *reinterpret_cast<double2*>(r0 + k) = make_double2(0.0, 0.0);
     const int slots[2] = {M.p_i[pi], M.p_j[pi]};
-    R Kc = 0.0;
+    R Kc[3] = {0.0, 0.0, 0.0};
     for (int s = 0; s < 2; ++s) {
       const R sg = s ? -1.0 : 1.0;
       const int sl = slots[s], bt = M.s_btype[sl], bi = M.s_body[sl];
@@ -652,33 +655,52 @@ __device__ __forceinline__ void substep(const Model& M, const BsSimParams& P, co
         for (int kk = bi; kk >= 0; kk = M.parent[kk]) {
           if (M.jtype[kk] == BS_JOINT_FIXED) continue;
           const V3<R> col = add(ld3(Sv + 6 * kk + 3), crs(ld3(Sv + 6 * kk), Pc));
-          J[M.dof[kk]] += sg * dot(dir, col);
+          const int jd = JI(M.dof[kk]);
+#pragma unroll
+          for (int t = 0; t < 3; ++t) r0[t * RW + jd] += sg * dot(dirs[t], col);
         }
       } else if (bt == BS_BODY_ACTOR) {
-        R* Jb = J + Dm + 6 * bi;
-        R* Wb = W + Dm + 6 * bi;
+        const int ub = Dm + 6 * bi;
         const R invm = 1.0 / M.a_mass[bi];
-        const V3<R> Jv = scl(dir, sg);
-        const V3<R> Jw = scl(crs(sub(Pc, ld3(E + Y.apose + 7 * bi)), dir), sg);
-        const V3<R> Wv = scl(Jv, invm);
-        const V3<R> Ww = m3mul(E + Y.Iwi + 9 * bi, Jw);
-        st3(Jb, Jv); st3(Jb + 3, Jw);
-        st3(Wb, Wv); st3(Wb + 3, Ww);
-        Kc += dot(dir, dir) * invm + dot(Jw, Ww);
+        const V3<R> lever = sub(Pc, ld3(E + Y.apose + 7 * bi));
+        const R* Iw = E + Y.Iwi + 9 * bi;
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+          const V3<R> Jv = scl(dirs[t], sg);
+          const V3<R> Jw = scl(crs(lever, dirs[t]), sg);
+          const V3<R> Wv = scl(Jv, invm);
+          const V3<R> Ww = m3mul(Iw, Jw);
+          R* rt = r0 + t * RW;
+          *reinterpret_cast<double2*>(rt + JI(ub + 0)) = make_double2(Jv.x, Wv.x);
+          *reinterpret_cast<double2*>(rt + JI(ub + 1)) = make_double2(Jv.y, Wv.y);
+          *reinterpret_cast<double2*>(rt + JI(ub + 2)) = make_double2(Jv.z, Wv.z);
+          *reinterpret_cast<double2*>(rt + JI(ub + 3)) = make_double2(Jw.x, Ww.x);
+          *reinterpret_cast<double2*>(rt + JI(ub + 4)) = make_double2(Jw.y, Ww.y);
+          *reinterpret_cast<double2*>(rt + JI(ub + 5)) = make_double2(Jw.z, Ww.z);
+          Kc[t] += dot(dirs[t], dirs[t]) * invm + dot(Jw, Ww);
+        }
       }
     }
-    R KA = 0.0;
-    for (int i = 0; i < D; ++i) {
-      R w = 0.0;
-      for (int k = 0; k < D; ++k) w += Minv[i * Dm + k] * J[k];
-      W[i] = w;
-      KA += J[i] * w;
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      R* rt = r0 + t * RW;
+      R KA = 0.0;
+      for (int i = 0; i < D; ++i) {
+        R w = 0.0;
+        for (int k = 0; k < D; ++k) w += Minv[i * Dm + k] * rt[JI(k)];
+        rt[WI(i)] = w;
+        KA += rt[JI(i)] * w;
+      }
+      Kc[t] = KA + Kc[t];
     }
-    Kc = KA + Kc;
-    row[0] = Kc > 1e-12 ? 1.0 / Kc : 0.0;
-    row[1] = 0.0;
-    row[2] = depth > slop ? P.beta * (depth - slop) / dt : (depth >= 0.0 ? 0.0 : depth / dt);
-    row[3] = depth < 0.0 ? depth / dt : 0.0;
+    const R tp = depth > slop ? P.beta * (depth - slop) / dt : (depth >= 0.0 ? 0.0 : depth / dt);
+    const R tv = depth < 0.0 ? depth / dt : 0.0;
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      R* rt = r0 + t * RW;
+      *reinterpret_cast<double2*>(rt) = make_double2(Kc[t] > 1e-12 ? 1.0 / Kc[t] : 0.0, 0.0);
+      *reinterpret_cast<double2*>(rt + 2) = make_double2(tp, tv);
+    }
   }
   __syncwarp();
   BS_TICK(12);
@@ -704,7 +726,7 @@ __device__ __forceinline__ void substep(const Model& M, const BsSimParams& P, co
     BS_COUNT(21, ncw);
     #pragma unroll 1
     for (int r = nrows; r < 3 * ncw; ++r)
-      for (int k = l; k < NU; k += G) rows[r * RW + ROW_J + NU + k] = 0.0;
+      for (int k = l; k < NU; k += G) rows[r * RW + WI(k)] = 0.0;
     __syncwarp();
     R u[NUM];
 #pragma unroll
@@ -720,13 +742,15 @@ __device__ __forceinline__ void substep(const Model& M, const BsSimParams& P, co
 #pragma unroll
         for (int t = 0; t < 3; ++t) {
           const R* rt = r0 + t * RW;
-          invK[t] = rt[0];
-          old[t] = rt[1];
+          const double2 h = *reinterpret_cast<const double2*>(rt);
+          invK[t] = h.x;
+          old[t] = h.y;
           act[t] = live && invK[t] != 0.0;
 #pragma unroll
           for (int j = 0; j < NUM; ++j) {
-            Jc[t][j] = j < NU ? rt[ROW_J + j] : 0.0;
-            Wc[t][j] = j < NU ? rt[ROW_J + NU + j] : 0.0;
+            const double2 jw = j < NU ? *reinterpret_cast<const double2*>(rt + JI(j)) : make_double2(0.0, 0.0);
+            Jc[t][j] = jw.x;
+            Wc[t][j] = jw.y;
           }
         }
         const R tgt = r0[tsel];
@@ -785,7 +809,7 @@ __device__ __forceinline__ void substep(const Model& M, const BsSimParams& P, co
 #pragma unroll
         for (int j = 0; j < KP; ++j) {
           const int k = l + PL * j;
-          if (owner && k < NU) { n_J[j] = rw[ROW_J + k]; n_W[j] = rw[ROW_J + NU + k]; }
+          if (owner && k < NU) { n_J[j] = rw[JI(k)]; n_W[j] = rw[WI(k)]; }
         }
       }
       R lam_n = 0.0;
@@ -802,7 +826,7 @@ __device__ __forceinline__ void substep(const Model& M, const BsSimParams& P, co
 #pragma unroll
           for (int j = 0; j < KP; ++j) {
             const int k = l + PL * j;
-            if (owner && k < NU) { n_J[j] = rw[ROW_J + k]; n_W[j] = rw[ROW_J + NU + k]; }
+            if (owner && k < NU) { n_J[j] = rw[JI(k)]; n_W[j] = rw[WI(k)]; }
           }
         }
         if (invK != 0.0) {
@@ -1131,21 +1155,27 @@ static Lay make_lay(const BsModelTables& T, int G) {
   y.goal = o; o += 3;
   y.lpq = o; o += 7 * y.Lm;
   y.Sv = o; o += 6 * y.Lm;
-  y.In = o; o += 10 * y.Lm;
-  y.Mt = o; o += y.Dm * y.Dm;
   y.Minv = o; o += y.Dm * y.Dm;
-  y.cb = o; o += y.Dm;
   y.u = o; o += y.Dm + 6 * y.Am;
   y.Iwi = o; o += 9 * y.Am;
-  y.spq = o; o += 7 * y.Sm;
   // union: {FK local transforms + RNEA temporaries} | {compacted contacts}
   const int fkr = 7 * y.Lm + 18 * y.Lm, cts = 8 * y.Cm;
   y.Tl = o; y.V = o + 7 * y.Lm; y.Ac = y.V + 6 * y.Lm; y.F = y.Ac + 6 * y.Lm;
   y.ct = o;
   o += fkr > cts ? fkr : cts;
+  o += o & 1;  // rows start 16-byte aligned
   y.rows = o;
+  // The row storage also holds the substep scratch that is dead before the rows are built:
+  // [0, 8 C_max) the narrowphase candidate slots (H), then the shape poses (A -> H), the mass
+  // matrix / Cholesky factor (A -> G), the bias forces (D -> G) and the world inertias (A -> E).
+  int r = 8 * y.Cm;
+  y.spq = o + r; r += 7 * y.Sm;
+  y.Mt = o + r; r += y.Dm * y.Dm;
+  y.cb = o + r; r += y.Dm;
+  y.In = o + r; r += 10 * y.Lm;
   const int rws = 3 * y.Cm * y.RW;
-  o += rws > 8 * y.Cm ? rws : 8 * y.Cm;  // row storage doubles as the candidate slots
+  o += rws > r ? rws : r;
+  o += o & 1;  // every env's block starts 16-byte aligned
   y.total = o;
   return y;
 }
@@ -1153,15 +1183,36 @@ static Lay make_lay(const BsModelTables& T, int G) {
 template <class K>
 static int launch(const BsModelTables& T, const BsEnvState& S, const BsStepOutputs& O, const BsSimParams& P,
                   const float* action, cudaStream_t st) {
-  const Lay y = make_lay(T, K::G);
+  Lay y = make_lay(T, K::G);
+  static size_t attr_bytes = 0;  // opt-in above 48 KB, raised on demand
+  auto ensure_attr = [](size_t b) {
+    if (b <= attr_bytes) return true;
+    if (cudaFuncSetAttribute(k_step<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b) != cudaSuccess)
+      return false;
+    attr_bytes = b;
+    return true;
+  };
+  // Pad the per-env stride to 2 (mod 16) doubles when that costs no residency: the groups of a
+  // warp then sit in distinct 16-byte bank slots for the sweep's broadcast loads.
+  static int last_key[5] = {-1, -1, -1, -1, -1}, last_total = 0;
+  const int key[5] = {y.Dm, y.Lm, y.Sm, y.Cm, y.Am};
+  if (memcmp(key, last_key, sizeof(key)) == 0) {
+    y.total = last_total;
+  } else {
+    const int padded = y.total + ((2 - y.total % 16) + 16) % 16;
+    const size_t b0 = (size_t)K::EPW * y.total * sizeof(double), b1 = (size_t)K::EPW * padded * sizeof(double);
+    if (b1 <= 220 * 1024 && ensure_attr(b1)) {
+      int n0 = 0, n1 = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n0, k_step<K>, 32, b0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n1, k_step<K>, 32, b1);
+      if (n1 >= n0) y.total = padded;
+    }
+    memcpy(last_key, key, sizeof(key));
+    last_total = y.total;
+  }
   const size_t bytes = (size_t)K::EPW * y.total * sizeof(double);
   if (bytes > 220 * 1024) return BS_ERR_UNSUPPORTED;
-  static size_t attr_bytes = 0;  // opt-in above 48 KB, raised on demand
-  if (bytes > attr_bytes) {
-    if (cudaFuncSetAttribute(k_step<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
-      return BS_ERR_CUDA;
-    attr_bytes = bytes;
-  }
+  if (!ensure_attr(bytes)) return BS_ERR_CUDA;
   const int blocks = (S.num_envs + K::EPW - 1) / K::EPW;
   k_step<K><<<blocks, 32, bytes, st>>>(T, S, O, P, action, y);
   return launch_status();
