@@ -97,7 +97,7 @@ enum { BS_PAIR_UNSUPPORTED = 0, BS_PAIR_SPHERE_PLANE = 1, BS_PAIR_BOX_PLANE = 2,
        BS_PAIR_SWAP = 16 };
 enum { BS_CTRL_PD_JOINT_POS = 0, BS_CTRL_PD_JOINT_DELTA_POS = 1, BS_CTRL_PD_EE_DELTA_POSE = 2,
        BS_CTRL_BASE_FORWARD_ROTATE = 3 };
-enum { BS_TASK_NONE = 0, BS_TASK_PICKCUBE = 1, BS_TASK_OPENCHAIN = 2 };
+enum { BS_TASK_NONE = 0, BS_TASK_PICKCUBE = 1, BS_TASK_OPENCHAIN = 2, BS_TASK_CARTPOLE = 3 };
 
 typedef struct BsModelTables {
   int32_t num_models, L_max, D_max, S_max, P_max, A_max, C_max;

@@ -296,3 +296,76 @@ class PickHeteroOracle:
 
     def link_poses(self):
         return [(idx, o.link_poses(), o) for idx, o in self.groups]
+
+
+class CartpoleOracle:
+    """CartpoleBalance (A-27): the cartpole fixture, slider driven by
+    pd_joint_delta_pos, hinge passive.  Reset: slider, hinge and both rates ~ U(-noise, noise)
+    from reset uniforms 0..3.  Per control step: streak = streak + 1 if |theta| < success_angle
+    else 0; success = streak >= success_steps; fail = |theta| > fail_angle or |x| > fail_x or
+    diverged; reward = cos(theta) (float32); obs = (x, x_dot, theta, theta_dot)."""
+
+    N_UNIFORMS = 8
+
+    def __init__(self, spec, desc, num_envs, seed, env_offset=0, cfg=None):
+        self.spec = spec
+        self.model = Model(desc)
+        self.cfg = cfg or E.SimConfig()
+        self.B = num_envs
+        self.seed = seed
+        self.env_ids = np.arange(env_offset, env_offset + num_envs, dtype=np.uint64)
+        m = self.model
+        D = m.D
+        slider = 0  # fixture order: dof 0 = slider (cart), dof 1 = hinge (pole)
+        kp, kd, fl = np.zeros(D), np.zeros(D), np.full(D, np.inf)
+        kp[slider], kd[slider], fl[slider] = spec.kp, spec.kd, spec.force_limit
+        self.drv = E.Drives(kp, kd, fl, np.zeros((num_envs, D)))
+        self.ctrl = type("Ctrl", (), {"mode": spec.control_mode, "dofs": [slider], "scale": spec.action_scale})()
+        self.reset_count = np.zeros(num_envs, np.uint64)
+        self.elapsed = np.zeros(num_envs, np.int32)
+        self.streak = np.zeros(num_envs, np.int32)
+        self.st = None
+        self.reset()
+
+    def reset(self, mask=None):
+        idx = np.arange(self.B) if mask is None else np.nonzero(mask)[0]
+        m = self.model
+        if self.st is None:
+            self.st = E.State(np.zeros((self.B, m.D)), np.zeros((self.B, m.D)), np.zeros((self.B, 0, 3)),
+                              np.zeros((self.B, 0, 4)), np.zeros((self.B, 0, 3)), np.zeros((self.B, 0, 3)),
+                              np.zeros(self.B, np.uint8))
+        if len(idx):
+            u = reset_uniforms(self.seed, self.env_ids[idx], self.reset_count[idx], self.N_UNIFORMS)
+            n = self.spec.init_noise
+            st = self.st
+            for i in range(2):
+                st.q[idx, i] = uniform(-n, n, u[:, i])
+                st.qd[idx, i] = uniform(-n, n, u[:, 2 + i])
+            st.diverged[idx] = 0
+            self.elapsed[idx] = 0
+            self.streak[idx] = 0
+        return self.obs()
+
+    def obs(self):
+        q, qd = self.st.q, self.st.qd
+        return np.stack([q[:, 0], qd[:, 0], q[:, 1], qd[:, 1]], -1).astype(np.float32)
+
+    def step(self, action):
+        s = self.spec
+        self.st = E.control_step(self.model, self.st, self.drv, self.ctrl, np.asarray(action), self.cfg)
+        x, th = self.st.q[:, 0], self.st.q[:, 1]
+        self.streak = np.where(np.abs(th) < s.success_angle, self.streak + 1, 0).astype(np.int32)
+        success = self.streak >= s.success_steps
+        fail = (np.abs(th) > s.fail_angle) | (np.abs(x) > s.fail_x) | (self.st.diverged != 0)
+        reward = np.cos(th).astype(np.float32)
+        self.elapsed += 1
+        terminated = success | fail
+        truncated = self.elapsed >= s.max_steps
+        info = {"success": success, "fail": fail}
+        done = terminated | truncated
+        final = {"q": self.st.q.copy(), "qd": self.st.qd.copy(), "streak": self.streak.copy(),
+                 "elapsed": self.elapsed.copy()}
+        if done.any():
+            self.reset_count[done] += 1
+            self.reset(done)
+        return self.obs(), reward, terminated, truncated, info, final

@@ -85,4 +85,4 @@ PAIR_CODE = {(0, 4): 1, (1, 4): 2, (0, 0): 3, (0, 1): 4, (2, 4): 5}
 PAIR_MAXC = {1: 1, 2: 4, 3: 1, 4: 1, 5: 2}
 PAIR_SWAP = 16
 CTRL = {"pd_joint_pos": 0, "pd_joint_delta_pos": 1, "pd_ee_delta_pose": 2, "base_forward_rotate": 3}
-TASK_NONE, TASK_PICKCUBE, TASK_OPENCHAIN = 0, 1, 2
+TASK_NONE, TASK_PICKCUBE, TASK_OPENCHAIN, TASK_CARTPOLE = 0, 1, 2, 3

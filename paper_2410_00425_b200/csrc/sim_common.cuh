@@ -206,7 +206,9 @@ __device__ __forceinline__ V3<R> m3mul(const R* A, V3<R> x) {
 
 // ---------------------------------------------------------------- tasks
 // PickCube task_f layout: 0 q_noise, 1 cube_half, 2 cube_xy, 3 goal_xy, 4 success_dist,
-// 5 fail_z, 6..8 q_rest.   OpenChain task_f: 0 success_frac.
+// 5 fail_z, 6..8 q_rest.   OpenChain task_f: 0 q_noise, 1 success_frac, 6..8 q_rest.
+// Cartpole task_f: 0 init_noise, 1 success_angle, 2 success_steps, 3 fail_angle, 4 fail_x
+// (dof 0 = slider, dof 1 = hinge; the per-env task integer holds the upright streak).
 
 // Reference-order quaternion product / normalisation with every operation rounded separately
 // (no FMA contraction even in FMA-enabled translation units): reset sampling must equal the
@@ -266,6 +268,14 @@ static __device__ __noinline__ void task_reset(const Model M, const BsSimParams&
     int pick = nobj > 0 ? 3 + min((int)(u[3] * nobj), nobj - 1) : -1;
     *target_dof = pick;
     goal[0] = goal[1] = goal[2] = 0.0;
+  } else if (P.task == BS_TASK_CARTPOLE) {
+    const R n = P.task_f[0];
+    for (int i = 0; i < 2 && i < M.D; ++i) {
+      q[i] = uni(-n, n, u[i]);
+      qd[i] = uni(-n, n, u[2 + i]);
+    }
+    *target_dof = 0;  // upright streak
+    goal[0] = goal[1] = goal[2] = 0.0;
   }
 }
 
@@ -302,8 +312,13 @@ static __device__ __forceinline__ void pack_obs(const Model& M, const BsSimParam
                          const V3<R>* lp, const V3<R>* ap, const Q4<R>* aq, const V3<R>* av,
                          const V3<R>* aw, const R* goal, float* o, int obs_dim) {
   // layout: q[D_max] qd[D_max] ee_p[3]
-  //   per actor slot: p[3] q[4] v[3] w[3]   goal[3]
+  //   per actor slot: p[3] q[4] v[3] w[3]   goal[3];  CartpoleBalance: (x, x_dot, theta, theta_dot)
   int k = 0;
+  if (P.task == BS_TASK_CARTPOLE) {
+    o[0] = (float)q[0]; o[1] = (float)qd[0]; o[2] = (float)q[1]; o[3] = (float)qd[1];
+    for (k = 4; k < obs_dim; ++k) o[k] = 0.0f;
+    return;
+  }
   for (int i = 0; i < Dm; ++i) o[k++] = i < M.D ? (float)q[i] : 0.0f;
   for (int i = 0; i < Dm; ++i) o[k++] = i < M.D ? (float)qd[i] : 0.0f;
   V3<R> ee = P.ee_link >= 0 ? lp[P.ee_link] : v3(0, 0, 0);

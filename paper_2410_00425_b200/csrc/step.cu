@@ -1045,6 +1045,12 @@ __global__ void __launch_bounds__(32) k_step(const __grid_constant__ BsModelTabl
     const R qv = tdof >= 0 ? E[Y.q + tdof] : 0.0;
     success = tdof >= 0 && qv > P.task_f[1] * hi;
     reward = (float)(tdof >= 0 ? qv / hi : 0.0);
+  } else if (P.task == BS_TASK_CARTPOLE) {
+    const R x = E[Y.q], th = E[Y.q + 1];
+    tdof = fabs(th) < P.task_f[1] ? tdof + 1 : 0;  // upright streak (control steps)
+    success = tdof >= (int32_t)P.task_f[2];
+    fail = fabs(th) > P.task_f[3] || fabs(x) > P.task_f[4] || diverged;
+    reward = (float)cos(th);
   }
   int32_t el = S.elapsed[e] + 1;
   const bool terminated = P.early_termination ? (success || fail) : false;
@@ -1056,6 +1062,7 @@ __global__ void __launch_bounds__(32) k_step(const __grid_constant__ BsModelTabl
     O.success[e] = success;
     O.fail[e] = fail;
     O.unsupported_pairs[e] = unsupported;
+    if (P.task == BS_TASK_CARTPOLE) S.target_dof[e] = tdof;
     // EpisodeMetrics: return = sum of rewards, *_once latch, *_at_end
     // sampled at the final step; emitted when the episode ends, accumulators restart.
     if (S.ep_return) {
@@ -1123,10 +1130,12 @@ __global__ void __launch_bounds__(32) k_step(const __grid_constant__ BsModelTabl
     //   per actor slot: p[3] q[4] v[3] w[3]   goal[3]   zero padding
     float* o = O.obs + (int64_t)e * O.obs_dim;
     const int b_ee = 2 * Dm, b_act = b_ee + 3, b_goal = b_act + 13 * Am;
+    const bool cart = P.task == BS_TASK_CARTPOLE;
     #pragma unroll 1
     for (int k = l; k < O.obs_dim; k += G) {
       R v = 0.0;
-      if (k < Dm) v = k < M.D ? E[Y.q + k] : 0.0;
+      if (cart) v = k < 4 ? E[(k & 1 ? Y.qd : Y.q) + (k >> 1)] : 0.0;
+      else if (k < Dm) v = k < M.D ? E[Y.q + k] : 0.0;
       else if (k < b_ee) v = (k - Dm) < M.D ? E[Y.qd + k - Dm] : 0.0;
       else if (k < b_act) v = P.ee_link >= 0 ? lpq[7 * P.ee_link + (k - b_ee)] : 0.0;
       else if (k < b_goal) {

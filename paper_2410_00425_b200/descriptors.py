@@ -95,6 +95,7 @@ class ControlSpec:
     force_limit: float = 100.0
     ik_lambda: float = 0.05
     action_scale_rot: float = 0.05   # pd_ee_delta_pose rotation, rad per unit action (A-22)
+    joints: tuple = ()               # joint subset by name; empty = every dof of `robot`
 
 
 @dataclass(frozen=True)
@@ -165,6 +166,43 @@ class OpenCabinetSpec:
 
     def control(self):
         return ControlSpec(self.control_mode, "arm", self.action_scale, self.kp, self.kd, self.force_limit)
+
+
+@dataclass(frozen=True)
+class CartpoleSpec:
+    """CartpoleBalance (PAPER.md A.10): the cartpole fixture (tasks/fixtures.py:154-176)
+    alone, the slider driven by pd_joint_delta_pos, the hinge passive.  Reset: slider, hinge and
+    both rates ~ U[-init_noise, init_noise].  Reward = cos(hinge angle) (upright cosine shaping).
+    Success = |angle| < success_angle on each of the trailing `success_steps` control steps (a
+    per-env streak counter).  Fail = |angle| > fail_angle or |slider| > fail_x (or divergence).
+    State obs = (x, x_dot, theta, theta_dot)."""
+
+    init_noise: float = 0.05
+    success_angle: float = 0.2
+    success_steps: int = 50
+    fail_angle: float = 0.8
+    fail_x: float = 1.7
+    max_steps: int = 200
+    control_mode: str = "pd_joint_delta_pos"
+    action_scale: float = 0.05
+    kp: float = 1000.0
+    kd: float = 2.0 * math.sqrt(1000.0)
+    force_limit: float = 100.0
+
+    def task_f(self):
+        return [self.init_noise, self.success_angle, float(self.success_steps), self.fail_angle, self.fail_x,
+                0.0, 0.0, 0.0, 0.0]
+
+    def control(self):
+        return ControlSpec(self.control_mode, "cartpole", self.action_scale, self.kp, self.kd, self.force_limit,
+                           joints=("slider",))
+
+
+def cartpole_desc(spec: CartpoleSpec) -> SceneDesc:
+    from . import fixtures as F
+    from .assets import load_mjcf
+
+    return SceneDesc((ArticulationDesc("cartpole", load_mjcf(F.CARTPOLE_MJCF)[0]),), (), ())
 
 
 TAG_SCENE = 0x5343454E  # 'SCEN': build-time per-env scene sampling stream

@@ -88,7 +88,8 @@ class Env:
             p.task_f[i] = v
         self.c_params = p
         N, dev = self.num_envs, self.device
-        self.obs_dim = 2 * scene.D_max + 3 + 13 * scene.A_max + 3
+        # state obs layout; CartpoleBalance: (x, x_dot, theta, theta_dot)
+        self.obs_dim = 4 if task == cabi.TASK_CARTPOLE else 2 * scene.D_max + 3 + 13 * scene.A_max + 3
         self.state_obs = torch.zeros((N, self.obs_dim), dtype=torch.float32, device=dev)
         self.reward = torch.zeros(N, dtype=torch.float32, device=dev)
         self.terminated = torch.zeros(N, dtype=torch.uint8, device=dev)

@@ -160,8 +160,8 @@ class PackedModel:
         self.kd = [0.0] * self.D
         self.flim = [math.inf] * self.D
         n = 0
-        for d, (_, _, art_name) in enumerate(self.dofs):
-            if art_name == control.robot:
+        for d, (_, j, art_name) in enumerate(self.dofs):
+            if art_name == control.robot and (not control.joints or j.name in control.joints):
                 self.ctrl[d] = n
                 self.kp[d], self.kd[d], self.flim[d] = control.kp, control.kd, control.force_limit
                 n += 1

@@ -7,6 +7,9 @@ Tasks on the hot path (BASELINE.json configs):
     -(|ee - cube| + |cube_xy - goal_xy|), time limit 100.
   * ``OpenCabinet`` -- ARM3 + a synthetic cabinet with per-env 2-6 drawers/doors (A-18,
     OpenChain-Hetero SPEC.md:615): success = target joint qpos > 0.9 * upper limit.
+  * ``PickHetero`` -- per-env object kind/size/colour and two jittered cameras (config C5).
+  * ``CartpoleBalance`` -- the cartpole fixture: slider driven, hinge passive,
+    reward cos(theta), success = upright for the trailing 50 steps, obs (x, x_dot, theta, theta_dot).
 """
 
 from __future__ import annotations
@@ -14,8 +17,8 @@ from __future__ import annotations
 from dataclasses import replace
 
 from . import cabi
-from .descriptors import (OpenCabinetSpec, PickCubeSpec, PickHeteroSpec, SceneDesc, hetero_descs,  # noqa: F401
-                          hetero_objects, opencabinet_descs, pickcube_desc)
+from .descriptors import (CartpoleSpec, OpenCabinetSpec, PickCubeSpec, PickHeteroSpec, SceneDesc,  # noqa: F401
+                          cartpole_desc, hetero_descs, hetero_objects, opencabinet_descs, pickcube_desc)
 from .envs import Env, SimConfig
 from .scene import build_batch
 
@@ -93,6 +96,24 @@ def _make_pickhetero(num_envs, seed, overrides, obs_mode, device, shard, sim, ca
               name="PickHetero", **kw)
     env.spec = spec
     env.descs = descs
+    env.reset()
+    return env
+
+
+@register("CartpoleBalance")
+def _make_cartpole(num_envs, seed, overrides, obs_mode, device, shard, sim, cameras, **kw):
+    from .cameras import CameraConfig, look_at, pinhole
+
+    spec = replace(CartpoleSpec(), **(overrides or {}))
+    scene = build_batch([cartpole_desc(spec)] * num_envs, seed, spec.control(), device, shard)
+    if obs_mode != "state" and cameras is None:
+        eye = (0.0, -3.0, 0.6)
+        cameras = [CameraConfig("front_camera", pose_p=eye, pose_q=look_at(eye, (0.0, 0.0, 0.3)),
+                                **pinhole(128, 128, 60.0))]
+    renderer = _renderer(scene, obs_mode, cameras, seed)
+    env = Env(scene, cabi.TASK_CARTPOLE, spec.task_f(), -1, spec.max_steps, seed, sim, obs_mode, renderer,
+              name="CartpoleBalance", **kw)
+    env.spec = spec
     env.reset()
     return env
 
