@@ -777,11 +777,14 @@ __device__ __forceinline__ void substep(const Model& M, const BsSimParams& P, co
 #pragma unroll
           for (int j = 0; j < NUM; ++j) u[j] = fma(delta, Wc[t][j], u[j]);
         }
+        __syncwarp();  // every lane has read the contact's multipliers (WAR)
 #pragma unroll
         for (int t = 0; t < 3; ++t)
           if (act[t]) r0[t * RW + 1] = nw[t];  // every lane stores the same value
+        __syncwarp();  // the stores are visible to every lane's next read of the row (RAW)
       }
     }
+    __syncwarp();  // every lane has read u from E before lane 0 overwrites it
 #pragma unroll
     for (int j = 0; j < NUM; ++j)
       if (l == 0 && j < NU) E[Y.u + j] = u[j];
@@ -848,7 +851,9 @@ __device__ __forceinline__ void substep(const Model& M, const BsSimParams& P, co
             nw = fmin(fmax(old + (0.0 - v) * invK, -bound), bound);
           }
           const R delta = nw - old;
-          if (owner) row[1] = nw;  // owner lanes store the same value and read back their own
+          __syncwarp(gmask);  // the group's lanes have read this row's multiplier (WAR)
+          if (owner) row[1] = nw;  // owner lanes store the same value
+          __syncwarp(gmask);  // visible to the group's next read of the row (RAW)
 #pragma unroll
           for (int j = 0; j < KP; ++j) u[j] += delta * Wc[j];
         } else if (rr == 0) {

@@ -1,3 +1,5 @@
+"""Repeated renders of random views vs the oracle (order-dependent raster bugs show up as sporadic
+bad frames).  Usage: python tools/raster_probe.py [reps] [tile]"""
 import sys, torch, numpy as np
 sys.path.insert(0, '.')
 sys.path.insert(0, 'tests')
