@@ -333,9 +333,10 @@ def measure(env, steps, warmup, flush, dist, local, seed_step=0):
 
 
 def measure_e2e(env, steps, dist, seed):
-    """The public API with host buffers: Env.step_host(host action) -- one CUDA graph with the
-    H2D copy of the action, the step (+ render) and the D2H copies of every obs tensor, the
-    reward and the flags -- then a stream synchronisation, every step."""
+    """The public API with host buffers: Env.step_host(host action) -- one CUDA graph in which
+    the step kernel reads the pinned host actions and writes obs / reward / flags to pinned host
+    memory over PCIe (zero-copy), plus the render and the D2H copies of the frames -- then a
+    stream synchronisation, every step."""
     import numpy as np
     import torch
 
@@ -389,8 +390,9 @@ def run_workload(name, steps, warmup, world, rank, local, dist, flush, seed, e2e
     e2e_s, h2d, d2h = measure_e2e(env, e2e_steps, dist, seed + rank)
     e2e = {"value": n_global * e2e_steps / e2e_s, "unit": "env-steps/s", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h, "steps": e2e_steps,
-           "path": "Env.step_host: one CUDA graph per step = H2D action + step (+ render) + D2H of every obs "
-                   "tensor, reward and flags; stream sync every step"}
+           "path": "Env.step_host: one CUDA graph per step = step kernel reading the pinned host actions and "
+                   "writing obs/reward/flags to pinned host memory over PCIe (zero-copy) (+ render + D2H of "
+                   "the frames); stream sync every step"}
     peak, peak_kind = _peaks()
     sim_b = sim_bytes_per_env_step(env.scene, env.obs_dim, env.action_dim)
     sim_s = m["sim_ms"] / 1e3 / steps

@@ -13,6 +13,7 @@ the next step) -- clone them to keep a history.
 from __future__ import annotations
 
 import ctypes
+import math
 from dataclasses import dataclass
 from typing import NamedTuple
 
@@ -90,12 +91,16 @@ class Env:
         N, dev = self.num_envs, self.device
         # state obs layout; CartpoleBalance: (x, x_dot, theta, theta_dot)
         self.obs_dim = 4 if task == cabi.TASK_CARTPOLE else 2 * scene.D_max + 3 + 13 * scene.A_max + 3
-        self.state_obs = torch.zeros((N, self.obs_dim), dtype=torch.float32, device=dev)
-        self.reward = torch.zeros(N, dtype=torch.float32, device=dev)
-        self.terminated = torch.zeros(N, dtype=torch.uint8, device=dev)
-        self.truncated = torch.zeros(N, dtype=torch.uint8, device=dev)
-        self.success = torch.zeros(N, dtype=torch.uint8, device=dev)
-        self.fail = torch.zeros(N, dtype=torch.uint8, device=dev)
+        # the per-step host-facing outputs (state obs, reward, four flag bytes) are views of ONE
+        # contiguous device arena, so the host-I/O path reads them back with a single copy
+        self._arena_layout = [("obs", (N, self.obs_dim), torch.float32), ("reward", (N,), torch.float32),
+                              ("terminated", (N,), torch.uint8), ("truncated", (N,), torch.uint8),
+                              ("success", (N,), torch.uint8), ("fail", (N,), torch.uint8)]
+        self._out_arena = torch.zeros(self._arena_bytes(), dtype=torch.uint8, device=dev)
+        v = self._arena_views(self._out_arena)
+        self.state_obs, self.reward = v["obs"], v["reward"]
+        self.terminated, self.truncated, self.success, self.fail = (v["terminated"], v["truncated"], v["success"],
+                                                                    v["fail"])
         self.unsupported = torch.zeros(N, dtype=torch.int32, device=dev)
         self.contact_count = torch.zeros(N, dtype=torch.int32, device=dev)
         self.contact_pairs = torch.zeros((N, scene.C_max, 2), dtype=torch.int32, device=dev)
@@ -225,13 +230,21 @@ class Env:
 
     # ------------------------------------------------------------------ host I/O path
     def enable_host_io(self, warmup: int = 2) -> None:
-        """Capture [H2D action, step, render, D2H obs/reward/flags] as ONE CUDA graph over pinned
-        host staging buffers, for callers that keep actions and observations on the host
-        (``step_host``).  The device-side API (``step``) is unaffected."""
+        """Capture [step reading the host actions and writing obs/reward/flags to host memory
+        (zero-copy over PCIe), render, D2H of the frames] as ONE CUDA graph over pinned host
+        buffers, for callers that keep actions and observations on the host (``step_host``).
+        The device-side API (``step``) is unaffected; in host-I/O steps the device copies of
+        obs/reward/flags are not written."""
         N, A = self.num_envs, max(1, self.action_dim)
         self._h_action = torch.zeros((N, A), dtype=torch.float32).pin_memory()
         outs = self._host_outputs()
-        self._h_outs = {k: torch.empty(v.shape, dtype=v.dtype).pin_memory() for k, v in outs.items()}
+        # the arena's tensors come back in one copy; frames (render modes) one copy each
+        self._h_arena = torch.zeros(self._out_arena.numel(), dtype=torch.uint8).pin_memory()
+        hv = self._arena_views(self._h_arena)
+        in_arena = {k: ("obs" if k in ("obs", "obs/state") else k) for k in outs
+                    if k in ("obs", "obs/state", "reward", "terminated", "truncated", "success", "fail")}
+        self._h_outs = {k: hv[in_arena[k]] if k in in_arena else torch.empty(v.shape, dtype=v.dtype).pin_memory()
+                        for k, v in outs.items()}
         s = torch.cuda.Stream(device=self.device)
         s.wait_stream(torch.cuda.current_stream(self.device))
         snap = self.scene.get_state()
@@ -239,14 +252,39 @@ class Env:
             for _ in range(warmup):
                 self._launch_step(self.action_buf.data_ptr())
         torch.cuda.current_stream(self.device).wait_stream(s)
+        # zero-copy: the step kernel reads the actions from, and writes obs / reward / flags to,
+        # the pinned host buffers directly over PCIe (page-locked memory is device-addressable
+        # under UVA), so the graph has no H2D/D2H copy nodes for them; frames are still copied
+        self._c_out_host = cabi.BsStepOutputs.from_buffer_copy(self.c_out)
+        for k in ("reward", "terminated", "truncated", "success", "fail"):
+            setattr(self._c_out_host, k, hv[k].data_ptr())
+        self._c_out_host.obs = hv["obs"].data_ptr()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            self.action_buf.copy_(self._h_action, non_blocking=True)
-            self._launch_step(self.action_buf.data_ptr())
+            nat.call("bs_step", ctypes.byref(self.scene.c_tables), ctypes.byref(self.scene.c_state),
+                     ctypes.byref(self._c_out_host), ctypes.byref(self.c_params), self._h_action.data_ptr(),
+                     nat.stream_handle())
+            self._render()
             for k, v in outs.items():
-                self._h_outs[k].copy_(v, non_blocking=True)
+                if k not in in_arena:
+                    self._h_outs[k].copy_(v, non_blocking=True)
         self.scene.set_state(snap)
         self._host_graph = g
+
+    def _arena_bytes(self) -> int:
+        n = 0
+        for _, shape, dt in self._arena_layout:
+            n = (n + 15) // 16 * 16 + math.prod(shape) * torch.empty(0, dtype=dt).element_size()
+        return (n + 15) // 16 * 16
+
+    def _arena_views(self, arena) -> dict:
+        out, n = {}, 0
+        for name, shape, dt in self._arena_layout:
+            n = (n + 15) // 16 * 16
+            nb = math.prod(shape) * torch.empty(0, dtype=dt).element_size()
+            out[name] = arena[n:n + nb].view(dt).view(shape)
+            n += nb
+        return out
 
     def _host_outputs(self) -> dict:
         out = {"reward": self.reward, "terminated": self.terminated, "truncated": self.truncated,
@@ -284,8 +322,9 @@ class Env:
 
     def host_io_bytes(self):
         """(H2D, D2H) bytes per step_host call."""
-        return (self._h_action.numel() * 4,
-                sum(v.numel() * v.element_size() for v in self._h_outs.values()))
+        frames = sum(v.numel() * v.element_size() for v in self._h_outs.values()
+                     if v.untyped_storage().data_ptr() != self._h_arena.untyped_storage().data_ptr())
+        return self._h_action.numel() * 4, self._h_arena.numel() + frames
 
     def _obs(self):
         if self.obs_mode == "state":

@@ -276,7 +276,8 @@ def test_episode_metrics_match_oracle(cuda):
 
 
 def test_step_host_matches_device_step(cuda):
-    """Env.step_host (one graph: H2D action, step, render, D2H outputs) == Env.step."""
+    """Env.step_host (one graph: step with zero-copy host actions and obs/reward/flags, render, D2H
+    frames) == Env.step, several steps in a row (auto-resets included)."""
     from paper_2410_00425_b200.tasks import make_task
 
     a = make_task("PickCube", 8, seed=17, obs_mode="rgbd")
@@ -287,6 +288,8 @@ def test_step_host_matches_device_step(cuda):
         ra = a.step(torch.as_tensor(act, device=a.device))
         hb = b.step_host(act)
         assert np.array_equal(ra.reward.cpu().numpy(), hb["reward"].numpy())
+        for k in ("terminated", "truncated", "success", "fail"):
+            assert np.array_equal(getattr(a, k).cpu().numpy(), hb[k].numpy()), k
         assert np.array_equal(ra.obs["state"].cpu().numpy(), hb["obs/state"].numpy())
         assert np.array_equal(ra.obs["sensor_data"]["base_camera"]["rgb"].cpu().numpy(),
                               hb["obs/sensor_data/base_camera/rgb"].numpy())
