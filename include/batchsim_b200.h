@@ -34,7 +34,7 @@ extern "C" {
 #define BS_ERR_UNSUPPORTED 6 /* ModelError      (errors.py:40) */
 
 /* ABI version: bumped whenever a signature or a struct layout below changes. */
-#define BS_ABI_VERSION 5
+#define BS_ABI_VERSION 6
 int bs_abi_version(void);
 
 /* Bind the library's CUDA runtime to `device` (call once per process/thread before use;
@@ -137,6 +137,8 @@ typedef struct BsModelTables {
   const double* actor_mass;    /* [M][A_max] */
   const double* actor_inertia; /* [M][A_max][3] principal, body frame            */
   const double* actor_rest;    /* [M][A_max][5] resting height z + orientation q (reset sampling) */
+  int32_t A_dyn;               /* max free actors of any model (<= A_max; may be 0 when A_max is
+                                  padded to 1): width of the step solver's actor block */
 } BsModelTables;
 
 typedef struct BsEnvState {

@@ -19,7 +19,7 @@ class BsModelTables(ctypes.Structure):
             "link_grounded", "link_axis", "link_org", "link_mass", "link_com", "link_inertia", "dof_lower",
             "dof_upper", "dof_damping", "dof_kp", "dof_kd", "dof_flim", "dof_ctrl", "shape_btype", "shape_body",
             "shape_kind", "shape_seg", "shape_size", "shape_frame", "shape_radius", "shape_color", "pair_i",
-            "pair_j", "pair_code", "pair_slot", "actor_mass", "actor_inertia", "actor_rest")]
+            "pair_j", "pair_code", "pair_slot", "actor_mass", "actor_inertia", "actor_rest")] + [("A_dyn", I32)]
 
 
 class BsEnvState(ctypes.Structure):

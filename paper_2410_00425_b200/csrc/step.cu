@@ -944,7 +944,9 @@ __global__ void __launch_bounds__(32) k_step(const __grid_constant__ BsModelTabl
   const int e = live ? e_raw : S.num_envs - 1;  // idle groups shadow the last env, never store
   R* E = smem + g * Y.total;
   const Model M = model_of(T, S.model_id[e]);
-  const int Dm = K::EXACT ? MD : Y.Dm, Am = K::EXACT ? MA : Y.Am;
+  // Am: the solver's actor block (smem staging, u, rows) = A_dyn; Ag: the actor stride of the
+  // global state rows and of the obs layout = A_max (A_dyn <= A_max)
+  const int Dm = K::EXACT ? MD : Y.Dm, Am = K::EXACT ? MA : Y.Am, Ag = K::EXACT ? MA : T.A_max;
   BS_TICK(0);
 
   // ---- stage the env's state rows
@@ -954,9 +956,9 @@ __global__ void __launch_bounds__(32) k_step(const __grid_constant__ BsModelTabl
     E[Y.qd + i] = S.qvel[(int64_t)e * Dm + i];
   }
   #pragma unroll 1
-  for (int i = l; i < 7 * Am; i += G) E[Y.apose + i] = S.actor_pose[(int64_t)e * 7 * Am + i];
+  for (int i = l; i < 7 * Am; i += G) E[Y.apose + i] = S.actor_pose[(int64_t)e * 7 * Ag + i];
   #pragma unroll 1
-  for (int i = l; i < 6 * Am; i += G) E[Y.avel + i] = S.actor_vel[(int64_t)e * 6 * Am + i];
+  for (int i = l; i < 6 * Am; i += G) E[Y.avel + i] = S.actor_vel[(int64_t)e * 6 * Ag + i];
   if (l < 3) E[Y.goal + l] = S.goal[3 * (int64_t)e + l];
   // ---- controller: drive targets, once per control step
   const float* act = action + (int64_t)e * P.action_dim;
@@ -1120,9 +1122,9 @@ __global__ void __launch_bounds__(32) k_step(const __grid_constant__ BsModelTabl
     if (i < M.D) S.target[(int64_t)e * Dm + i] = E[Y.tgt + i];
   }
   #pragma unroll 1
-  for (int i = l; i < 7 * M.A; i += G) S.actor_pose[(int64_t)e * 7 * Am + i] = E[Y.apose + i];
+  for (int i = l; i < 7 * M.A; i += G) S.actor_pose[(int64_t)e * 7 * Ag + i] = E[Y.apose + i];
   #pragma unroll 1
-  for (int i = l; i < 6 * M.A; i += G) S.actor_vel[(int64_t)e * 6 * Am + i] = E[Y.avel + i];
+  for (int i = l; i < 6 * M.A; i += G) S.actor_vel[(int64_t)e * 6 * Ag + i] = E[Y.avel + i];
   if (l < 3) S.goal[3 * (int64_t)e + l] = E[Y.goal + l];
   #pragma unroll 1
   for (int i = l; i < 7 * M.L; i += G) S.link_pose[(int64_t)e * 7 * Y.Lm + i] = lpq[i];
@@ -1134,7 +1136,7 @@ __global__ void __launch_bounds__(32) k_step(const __grid_constant__ BsModelTabl
     // layout: q[D_max] qd[D_max] ee_p[3]
     //   per actor slot: p[3] q[4] v[3] w[3]   goal[3]   zero padding
     float* o = O.obs + (int64_t)e * O.obs_dim;
-    const int b_ee = 2 * Dm, b_act = b_ee + 3, b_goal = b_act + 13 * Am;
+    const int b_ee = 2 * Dm, b_act = b_ee + 3, b_goal = b_act + 13 * Ag;
     const bool cart = P.task == BS_TASK_CARTPOLE;
     #pragma unroll 1
     for (int k = l; k < O.obs_dim; k += G) {
@@ -1156,7 +1158,8 @@ __global__ void __launch_bounds__(32) k_step(const __grid_constant__ BsModelTabl
 // ------------------------------------------------------------------ host side
 static Lay make_lay(const BsModelTables& T, int G) {
   Lay y;
-  y.Dm = T.D_max; y.Lm = T.L_max; y.Sm = T.S_max; y.Cm = T.C_max; y.Am = T.A_max;
+  y.Dm = T.D_max; y.Lm = T.L_max; y.Sm = T.S_max; y.Cm = T.C_max;
+  y.Am = T.A_dyn >= 0 && T.A_dyn < T.A_max ? T.A_dyn : T.A_max;  // solver actor block (A-dyn <= A_max)
   y.NU = y.Dm + 6 * y.Am;
   y.RW = ROW_J + 2 * y.NU;
   y.KCH = (y.Cm + G - 1) / G;
@@ -1270,7 +1273,8 @@ int bs_step(const BsModelTables* T, const BsEnvState* S, const BsStepOutputs* O,
     const char* v = getenv("BS_STEP_GENERIC");  // tests: force the runtime-width variants
     return v && atoi(v) != 0;
   }();
-  if (!generic && T->D_max == CfgPick::MD && T->A_max == CfgPick::MA) return launch<CfgPick>(*T, *S, *O, *P, action, st);
+  if (!generic && T->D_max == CfgPick::MD && T->A_max == CfgPick::MA && T->A_dyn == CfgPick::MA)
+    return launch<CfgPick>(*T, *S, *O, *P, action, st);
   if (T->D_max <= CfgSmall::MD && T->A_max <= CfgSmall::MA) return launch<CfgSmall>(*T, *S, *O, *P, action, st);
   if (T->D_max <= CfgArt::MD && T->A_max <= CfgArt::MA) return launch<CfgArt>(*T, *S, *O, *P, action, st);
   if (T->D_max <= CfgLarge::MD && T->A_max <= CfgLarge::MA) return launch<CfgLarge>(*T, *S, *O, *P, action, st);

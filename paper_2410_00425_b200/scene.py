@@ -290,6 +290,7 @@ class SceneBatch:
         ct = cabi.BsModelTables()
         ct.num_models, ct.L_max, ct.D_max, ct.S_max = M, Lm, Dm, Sm
         ct.P_max, ct.A_max, ct.C_max = Pm, Am, self.C_max
+        ct.A_dyn = max(m.A for m in self.models)  # 0 when no model has a free actor (A_max is padded to 1)
         for k, v in self.tables.items():
             setattr(ct, k, v.data_ptr())
         self.c_tables = ct

@@ -2,7 +2,7 @@
 
 Run on a GPU box (it rebuilds the library with -DBS_PHASE_TIMING first):
 
-    python tools/phase_timing.py [envs] [steps]
+    python tools/phase_timing.py [envs] [steps] [task]
 
 Thread 0 of CTA 0 records clock64() deltas at each phase boundary of k_step. Every env's step
 runs the same phase sequence and the kernel is latency-bound (k_step time is flat from 1024 to
@@ -39,7 +39,8 @@ def main():
     from paper_2410_00425_b200 import _native as nat
     from paper_2410_00425_b200.tasks import make_task
 
-    env = make_task("PickCube", envs, seed=0)
+    task = sys.argv[3] if len(sys.argv) > 3 else "PickCube"
+    env = make_task(task, envs, seed=0)
     for k in range(5):
         env.step_random(k)
     torch.cuda.synchronize()
@@ -52,12 +53,12 @@ def main():
     vals = {i: buf[i] / steps for i in range(18)}
     vals[0] = 0.0  # the first tick of a launch measures the gap since the previous launch
     tot = sum(vals.values())
-    out = {"envs": envs, "steps": steps, "cycles_per_step": tot,
+    out = {"task": task, "envs": envs, "steps": steps, "cycles_per_step": tot,
            "phases": {NAMES[i]: {"cycles": v, "share": v / tot} for i, v in vals.items() if i in NAMES}}
     for i, v in sorted(vals.items(), key=lambda x: -x[1]):
         print(f"{v:10.0f} cyc  {100 * v / tot:5.1f}%  {NAMES.get(i, i)}")
     print(f"total {tot:.0f} cycles per step ({tot / 1.965e3:.1f} us at 1965 MHz)")
-    subs = 2 * steps  # substeps per step (PickCube: sim 120 Hz / control 60 Hz)
+    subs = 2 * steps  # substeps per step (sim 120 Hz / control 60 Hz)
     out["contacts_env0_per_substep"] = buf[20] / subs
     out["contacts_warp_max_per_substep"] = buf[21] / subs
     print(f"contacts per substep: env0 {buf[20] / subs:.2f}, warp max {buf[21] / subs:.2f}")
