@@ -1,5 +1,8 @@
 """Developer tool: per-phase clocks of the rasterizer (k_render) on the C3 workload.
 
+Each phase time is thread 0's clock between consecutive phase barriers (BAR.SYNC may let the
+clock read issue before the barrier resolves, so a phase can absorb the previous one's tail).
+
 Run on a GPU box; rebuilds the library with -DBS_PHASE_TIMING (thread 0 of CTAs (0, 0),
 (0, 511), (0, 1023) print clock64() deltas at each phase barrier), renders a few C3 frames
 batches and prints the mean cycles per phase.  Rebuild normally afterwards.
@@ -12,8 +15,9 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-NAMES = ["transforms", "vertices", "triangles+live", "tile clear", "classify", "rows+tiny+pixels",
-         "resolve after 1st iteration", "resolve 1st iteration (thread 0)"]
+NAMES = {1: "transforms", 2: "vertices", 3: "triangles+live", 4: "tile clear", 5: "classify",
+         0: "tiny + row spans (4a)", 6: "scan + span walk (4b, 4c)", 7: "resolve"}
+ORDER = [1, 2, 3, 4, 5, 0, 6, 7]
 
 CHILD = r'''
 import sys, torch
@@ -52,11 +56,14 @@ def main():
         print(out)
         raise SystemExit("no RTCLK lines")
     n = len(rows)
-    mean = [sum(r[k + 1] for r in rows) / n for k in range(8)]
-    tot = sum(mean)
+    # RTCLK columns: marks 1..7 then 0
+    col = {k: k for k in range(1, 8)}
+    col[0] = 8
+    mean = {k: sum(r[col[k]] for r in rows) / n for k in ORDER}
+    tot = sum(mean.values())
     print(f"{cfg}: {n} samples, {tot:.0f} cycles per frame ({tot / 1.965e3:.1f} us at 1965 MHz)")
-    for name, v in zip(NAMES, mean):
-        print(f"  {name:20s} {v:9.0f} cycles  {100 * v / tot:5.1f}%")
+    for k in ORDER:
+        print(f"  {NAMES[k]:28s} {mean[k]:9.0f} cycles  {100 * mean[k] / tot:5.1f}%")
     if os.environ.get("BS_KEEP_TIMING_BUILD") is None:
         subprocess.run([sys.executable, "-m", "paper_2410_00425_b200.build_native", "--force"], check=True,
                        env={k: v for k, v in os.environ.items() if k != "BS_PHASE_TIMING"}, cwd=ROOT)
