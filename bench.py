@@ -327,7 +327,8 @@ def measure(env, steps, warmup, flush, dist, local, seed_step=0):
                       sum(e[2].elapsed_time(e[3]) for e in ev)], dtype=torch.float64, device=env.device)
     if dist is not None:
         _allreduce(dist, t, dist.ReduceOp.MAX)
-    launches = 2 + (len(env.renderer.groups) if env.renderer is not None else 0)
+    # k_random_actions + k_step, and per camera group k_frame_setup + k_render
+    launches = 2 + (2 * len(env.renderer.groups) if env.renderer is not None else 0)
     return {"step_ms": float(t[0]), "sim_ms": float(t[1]), "render_ms": float(t[2]), "clocks": clk.summary(),
             "launches": launches * steps}
 

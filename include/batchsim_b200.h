@@ -34,7 +34,7 @@ extern "C" {
 #define BS_ERR_UNSUPPORTED 6 /* ModelError      (errors.py:40) */
 
 /* ABI version: bumped whenever a signature or a struct layout below changes. */
-#define BS_ABI_VERSION 6
+#define BS_ABI_VERSION 7
 int bs_abi_version(void);
 
 /* Bind the library's CUDA runtime to `device` (call once per process/thread before use;
@@ -262,7 +262,10 @@ typedef struct BsRenderParams {
   double light_dir[3];         /* unit vector towards the light, world frame */
   float ambient, diffuse;      /* flat shading: ambient + diffuse * max(0, n.l) (A-12) */
   float background[3];         /* rgb in [0,1] of empty pixels */
-  int32_t tile;                /* CTA tile edge in pixels (0 = default 64) */
+  int32_t tile;                /* CTA tile edge in pixels (0 = default 128) */
+  float* frame_scratch;        /* optional device scratch [N][C][12 S_max + 20] floats: per-frame
+                                  shape -> camera transforms and camera block, computed by a
+                                  parallel pre-pass (NULL: computed inside the rasterizer) */
 } BsRenderParams;
 
 /* FrameBatch + the fused pointcloud (A-10).  Any pointer

@@ -17,7 +17,7 @@ from .errors import raise_for_status
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_lib", "libbatchsim_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "batchsim_b200.h")
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64

@@ -120,6 +120,11 @@ class Renderer:
 
         rp.ambient, rp.diffuse = params.ambient, params.diffuse
         rp.tile = int(os.environ.get("BS_RENDER_TILE", params.tile))  # CTA tile edge (perf knob)
+        # device scratch for the per-frame transform pre-pass (k_frame_setup), sized for the
+        # largest camera group; groups render one after another on the same stream
+        frames = max(N * len(g["cams"]) for g in self.groups)
+        self.frame_scratch = torch.empty(frames * (12 * scene.S_max + 20), dtype=torch.float32, device=dev)
+        rp.frame_scratch = self.frame_scratch.data_ptr()
         self.c_params = rp
         self.light = L
         self.env_color = None
