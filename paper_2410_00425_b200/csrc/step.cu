@@ -624,17 +624,19 @@ __device__ __forceinline__ void substep(const Model& M, const BsSimParams& P, co
   }
   __syncwarp();
   BS_TICK(11);
-  // ---- J: constraint rows.  One lane per contact builds its normal and two tangent rows
-  //         (shared slots, lever arms and chain walk; three independent reciprocals).
+  // ---- J: constraint rows.  One lane per (contact, row): the normal and the two tangent rows of
+  //         a contact are built by different lanes (shared slots, lever arms and chain walk);
+  //         every lane recomputes the contact's tangent basis, so the rows stay independent.
   R* rows = E + Y.rows;
   const int NU = K::EXACT ? K::NU : Y.NU, RW = ROW_J + 2 * NU;
   #pragma unroll 1
-  for (int c = l; c < nc; c += G) {
+  for (int item = l; item < 3 * nc; item += G) {
+    const int c = item / 3, t = item - 3 * c;
     const R* cc = ct + 8 * c;
     const V3<R> Pc = ld3(cc), n = ld3(cc + 3);
     const R depth = cc[6];
     const int pi = (int)cc[7];
-    V3<R> dirs[3];
+    V3<R> dir;
     {  // tangent basis (A-6): t1 = normalize(n x e_k), e_k the least-aligned axis; t2 = n x t1
       const R an[3] = {fabs(n.x), fabs(n.y), fabs(n.z)};
       int k = 0;
@@ -642,12 +644,12 @@ __device__ __forceinline__ void substep(const Model& M, const BsSimParams& P, co
       if (an[2] < an[k]) k = 2;
       V3<R> t1 = crs(n, v3(k == 0, k == 1, k == 2));
       t1 = scl(t1, rsqrt(dot(t1, t1)));
-      dirs[0] = n; dirs[1] = t1; dirs[2] = crs(n, t1);
+      dir = t == 0 ? n : (t == 1 ? t1 : crs(n, t1));
     }
-    R* r0 = rows + 3 * c * RW;
-    for (int k = 0; k < 3 * RW; k += 2) *reinterpret_cast<double2*>(r0 + k) = make_double2(0.0, 0.0);
+    R* rt = rows + (3 * c + t) * RW;
+    for (int k = 0; k < RW; k += 2) *reinterpret_cast<double2*>(rt + k) = make_double2(0.0, 0.0);
     const int slots[2] = {M.p_i[pi], M.p_j[pi]};
-    R Kc[3] = {0.0, 0.0, 0.0};
+    R Kc = 0.0;
     for (int s = 0; s < 2; ++s) {
       const R sg = s ? -1.0 : 1.0;
       const int sl = slots[s], bt = M.s_btype[sl], bi = M.s_body[sl];
@@ -655,52 +657,38 @@ __device__ __forceinline__ void substep(const Model& M, const BsSimParams& P, co
         for (int kk = bi; kk >= 0; kk = M.parent[kk]) {
           if (M.jtype[kk] == BS_JOINT_FIXED) continue;
           const V3<R> col = add(ld3(Sv + 6 * kk + 3), crs(ld3(Sv + 6 * kk), Pc));
-          const int jd = JI(M.dof[kk]);
-#pragma unroll
-          for (int t = 0; t < 3; ++t) r0[t * RW + jd] += sg * dot(dirs[t], col);
+          rt[JI(M.dof[kk])] += sg * dot(dir, col);
         }
       } else if (bt == BS_BODY_ACTOR) {
         const int ub = Dm + 6 * bi;
         const R invm = 1.0 / M.a_mass[bi];
         const V3<R> lever = sub(Pc, ld3(E + Y.apose + 7 * bi));
         const R* Iw = E + Y.Iwi + 9 * bi;
-#pragma unroll
-        for (int t = 0; t < 3; ++t) {
-          const V3<R> Jv = scl(dirs[t], sg);
-          const V3<R> Jw = scl(crs(lever, dirs[t]), sg);
-          const V3<R> Wv = scl(Jv, invm);
-          const V3<R> Ww = m3mul(Iw, Jw);
-          R* rt = r0 + t * RW;
-          *reinterpret_cast<double2*>(rt + JI(ub + 0)) = make_double2(Jv.x, Wv.x);
-          *reinterpret_cast<double2*>(rt + JI(ub + 1)) = make_double2(Jv.y, Wv.y);
-          *reinterpret_cast<double2*>(rt + JI(ub + 2)) = make_double2(Jv.z, Wv.z);
-          *reinterpret_cast<double2*>(rt + JI(ub + 3)) = make_double2(Jw.x, Ww.x);
-          *reinterpret_cast<double2*>(rt + JI(ub + 4)) = make_double2(Jw.y, Ww.y);
-          *reinterpret_cast<double2*>(rt + JI(ub + 5)) = make_double2(Jw.z, Ww.z);
-          Kc[t] += dot(dirs[t], dirs[t]) * invm + dot(Jw, Ww);
-        }
+        const V3<R> Jv = scl(dir, sg);
+        const V3<R> Jw = scl(crs(lever, dir), sg);
+        const V3<R> Wv = scl(Jv, invm);
+        const V3<R> Ww = m3mul(Iw, Jw);
+        *reinterpret_cast<double2*>(rt + JI(ub + 0)) = make_double2(Jv.x, Wv.x);
+        *reinterpret_cast<double2*>(rt + JI(ub + 1)) = make_double2(Jv.y, Wv.y);
+        *reinterpret_cast<double2*>(rt + JI(ub + 2)) = make_double2(Jv.z, Wv.z);
+        *reinterpret_cast<double2*>(rt + JI(ub + 3)) = make_double2(Jw.x, Ww.x);
+        *reinterpret_cast<double2*>(rt + JI(ub + 4)) = make_double2(Jw.y, Ww.y);
+        *reinterpret_cast<double2*>(rt + JI(ub + 5)) = make_double2(Jw.z, Ww.z);
+        Kc += dot(dir, dir) * invm + dot(Jw, Ww);
       }
     }
-#pragma unroll
-    for (int t = 0; t < 3; ++t) {
-      R* rt = r0 + t * RW;
-      R KA = 0.0;
-      for (int i = 0; i < D; ++i) {
-        R w = 0.0;
-        for (int k = 0; k < D; ++k) w += Minv[i * Dm + k] * rt[JI(k)];
-        rt[WI(i)] = w;
-        KA += rt[JI(i)] * w;
-      }
-      Kc[t] = KA + Kc[t];
+    R KA = 0.0;
+    for (int i = 0; i < D; ++i) {
+      R w = 0.0;
+      for (int k = 0; k < D; ++k) w += Minv[i * Dm + k] * rt[JI(k)];
+      rt[WI(i)] = w;
+      KA += rt[JI(i)] * w;
     }
+    Kc = KA + Kc;
     const R tp = depth > slop ? P.beta * (depth - slop) / dt : (depth >= 0.0 ? 0.0 : depth / dt);
     const R tv = depth < 0.0 ? depth / dt : 0.0;
-#pragma unroll
-    for (int t = 0; t < 3; ++t) {
-      R* rt = r0 + t * RW;
-      *reinterpret_cast<double2*>(rt) = make_double2(Kc[t] > 1e-12 ? 1.0 / Kc[t] : 0.0, 0.0);
-      *reinterpret_cast<double2*>(rt + 2) = make_double2(tp, tv);
-    }
+    *reinterpret_cast<double2*>(rt) = make_double2(Kc > 1e-12 ? 1.0 / Kc : 0.0, 0.0);
+    *reinterpret_cast<double2*>(rt + 2) = make_double2(tp, tv);
   }
   __syncwarp();
   BS_TICK(12);
