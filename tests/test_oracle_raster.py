@@ -109,3 +109,13 @@ def test_greenscreen_kats():
     seg[:, :4] = 3
     out = raster.composite_greenscreen(rgb, seg, bg)
     assert np.array_equal(out[:, :4], rgb[:, :4]) and np.array_equal(out[:, 4:], bg[:, 4:])
+
+
+def test_u8_unit_division_free_form_matches_numpy():
+    """csrc/raster.cu u8_unit: c * (1/255) plus one residual correction, each op rounded in
+    float32, equals numpy's float32 c / 255 for every c in [0, 255] (the pointcloud colours)."""
+    c = np.arange(256, dtype=np.float32)
+    k = np.float32(1) / np.float32(255)
+    b = c * k
+    got = b + (c - b * np.float32(255)) * k
+    assert np.array_equal(got.view(np.uint32), (c / np.float32(255)).view(np.uint32))
