@@ -1018,6 +1018,7 @@ __global__ void __launch_bounds__(32) k_step(const __grid_constant__ BsModelTabl
       if (l == 0) O.contact_count[e] = nc;
     }
   }
+  __syncwarp();  // the contact export reads the compacted contacts that the FK scratch aliases
   fk_group<G>(M, Y, E, l);
   BS_TICK(15);
 
