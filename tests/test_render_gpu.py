@@ -109,6 +109,31 @@ def test_graph_replay_renders_like_eager(cuda):
         assert np.array_equal(fa[k], fb[k]), k
 
 
+def test_frame_setup_prepass_equals_in_kernel_transforms(cuda):
+    """ABI 7: the k_frame_setup pre-pass (BsRenderParams.frame_scratch) and the rasterizer's own
+    in-kernel transforms (frame_scratch = NULL) give identical frames, pointcloud included."""
+    from paper_2410_00425_b200.tasks import make_task
+
+    env = make_task("PickCube", 5, seed=8, obs_mode="pointcloud")
+    for t in range(3):
+        env.step_random(t)
+    R, g = env.renderer, env.renderer.groups[0]
+    R.render()
+    torch.cuda.synchronize()
+    want = {k: g[k].clone() for k in ("rgb", "depth", "seg", "pc")}
+    keep = R.c_params.frame_scratch
+    try:
+        R.c_params.frame_scratch = None
+        for k in want:
+            g[k].zero_()
+        R.render()
+        torch.cuda.synchronize()
+    finally:
+        R.c_params.frame_scratch = keep
+    for k, v in want.items():
+        assert torch.equal(g[k].view(torch.uint8) if k == "rgb" else g[k], v), k
+
+
 def box_scene(n=2):
     from paper_2410_00425_b200.descriptors import ActorDesc, ControlSpec, SceneDesc
     from paper_2410_00425_b200.scene import build_batch
