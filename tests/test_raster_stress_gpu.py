@@ -105,3 +105,18 @@ def test_random_views_all_tiles_bit_exact(cuda, res, obs_mode):
             hit_counts.append(int((w_seg != 0).sum()))
     # the random views are not all empty: most frames see something, some are mostly covered
     assert np.mean(np.asarray(hit_counts) > 0) > 0.5 and max(hit_counts) > 0.5 * w * h
+
+
+@pytest.mark.parametrize("caps,obs_mode", [("4,16", "rgbd"), ("1,1", "pointcloud"), ("256,64", "rgbd")])
+def test_overflow_paths_bit_exact(cuda, caps, obs_mode):
+    """With the big-record and span capacities lowered (BS_RENDER_CAPS, a test knob read once per
+    process), triangles past the record capacity are drawn in-thread at classification and
+    spans past the list capacity are drawn in-lane -- frames must still equal the oracle."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, os.path.join(here, "raster_caps_child.py"), obs_mode],
+                       env=dict(os.environ, BS_RENDER_CAPS=caps), capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
