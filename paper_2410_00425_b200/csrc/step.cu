@@ -495,21 +495,28 @@ __device__ __forceinline__ void substep(const Model& M, const BsSimParams& P, co
   }
   __syncwarp();
   BS_TICK(5);
-  // ---- D: backward pass: bias forces C(q, qd) and composite inertias
-  if (l == 0) {
+  // ---- D: backward pass: bias forces C(q, qd) and composite inertias.  Both accumulations are
+  //         component-wise (child into parent, reverse topological order): lanes 0-5 carry one
+  //         force component each, lanes 6-7 five inertia components each; then the bias terms
+  //         S_k . F_k in parallel over links.
+  if (l < 6) {
     for (int k = L - 1; k >= 0; --k) {
-      const V6 Fk = ld6(F + 6 * k);
-      if (M.jtype[k] != BS_JOINT_FIXED) cb[M.dof[k]] = dot6(ld6(Sv + 6 * k), Fk);
+      const int par = M.parent[k];
+      if (par >= 0) F[6 * par + l] += F[6 * k + l];
+    }
+  } else if (l < 8) {
+    for (int k = L - 1; k >= 0; --k) {
       const int par = M.parent[k];
       if (par >= 0) {
-        st6(F + 6 * par, add6(ld6(F + 6 * par), Fk));
-        R* ip = In + 10 * par;
-        const R* ik = In + 10 * k;
 #pragma unroll
-        for (int j = 0; j < 10; ++j) ip[j] += ik[j];
+        for (int j = l - 6; j < 10; j += 2) In[10 * par + j] += In[10 * k + j];
       }
     }
   }
+  __syncwarp();
+  #pragma unroll 1
+  for (int k = l; k < L; k += G)
+    if (M.jtype[k] != BS_JOINT_FIXED) cb[M.dof[k]] = dot6(ld6(Sv + 6 * k), ld6(F + 6 * k));
   __syncwarp();
   BS_TICK(6);
   // ---- E: CRBA mass matrix (parallel over dof links)
