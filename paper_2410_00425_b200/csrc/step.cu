@@ -50,7 +50,21 @@ __device__ long long g_bs_last;
   do {                                                                         \
     if (blockIdx.x == 0 && threadIdx.x == 0) g_bs_phase[id] += (unsigned long long)(v); \
   } while (0)
+// every CTA: its own duration (slots 22 max, 23 sum, 24 count) -- the launch is as long as its
+// slowest warp, not env 0's
+#define BS_CTA_BEGIN const long long bs_cta_t0_ = clock64()
+#define BS_CTA_END                                                             \
+  do {                                                                         \
+    if (threadIdx.x == 0) {                                                    \
+      const unsigned long long d_ = (unsigned long long)(clock64() - bs_cta_t0_); \
+      atomicMax(&g_bs_phase[22], d_);                                          \
+      atomicAdd(&g_bs_phase[23], d_);                                          \
+      atomicAdd(&g_bs_phase[24], 1ull);                                        \
+    }                                                                          \
+  } while (0)
 #else
+#define BS_CTA_BEGIN do { } while (0)
+#define BS_CTA_END do { } while (0)
 #define BS_TICK(id) do { } while (0)
 #define BS_COUNT(id, v) do { } while (0)
 #endif
@@ -943,6 +957,7 @@ __global__ void __launch_bounds__(32) k_step(const __grid_constant__ BsModelTabl
   // global state rows and of the obs layout = A_max (A_dyn <= A_max)
   const int Dm = K::EXACT ? MD : Y.Dm, Am = K::EXACT ? MA : Y.Am, Ag = K::EXACT ? MA : T.A_max;
   BS_TICK(0);
+  BS_CTA_BEGIN;
 
   // ---- stage the env's state rows
   #pragma unroll 1
@@ -1149,6 +1164,7 @@ __global__ void __launch_bounds__(32) k_step(const __grid_constant__ BsModelTabl
     }
   }
   BS_TICK(17);
+  BS_CTA_END;
 }
 
 // ------------------------------------------------------------------ host side

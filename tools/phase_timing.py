@@ -62,6 +62,11 @@ def main():
     out["contacts_env0_per_substep"] = buf[20] / subs
     out["contacts_warp_max_per_substep"] = buf[21] / subs
     print(f"contacts per substep: env0 {buf[20] / subs:.2f}, warp max {buf[21] / subs:.2f}")
+    if buf[24]:
+        mean_cta = buf[23] / buf[24]
+        print(f"per-CTA duration over all launches: mean {mean_cta:.0f} cycles, max {buf[22]:.0f} cycles "
+              f"({buf[22] / 1.965e3:.1f} us) -- the launch lasts as long as its slowest warp")
+        out["cta_cycles_mean"], out["cta_cycles_max"] = mean_cta, buf[22]
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", "phase_timing.json"), "w") as f:
         json.dump(out, f, indent=1)
