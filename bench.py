@@ -44,7 +44,16 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
-METRIC = "env-steps/s (sim+render, whole box)"
+def _baseline_metric() -> str:
+    """The metric string exactly as BASELINE.json names it."""
+    try:
+        with open(os.path.join(ROOT, "BASELINE.json")) as f:
+            return json.load(f)["metric"]
+    except (OSError, KeyError, ValueError):
+        return "env-steps/s (sim+render, whole box) at 1/2/4/8 B200 vs reference CPU host cores"
+
+
+METRIC = _baseline_metric()
 FALLBACK_HBM_GBS = 6650.0
 WORKLOADS = {
     "c2": {"task": "PickCube", "envs": 4096, "obs_mode": "state",
