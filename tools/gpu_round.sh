@@ -1,6 +1,7 @@
 #!/bin/bash
 # One GPU session: GPU tests, bench (ours + reference arm), launch list, ncu captures of the
-# step and render kernels.  Usage (under gpurun): bash tools/gpu_round.sh [tag] [skip-ref]
+# step and render kernels.  Usage (under gpurun): bash tools/gpu_round.sh [tag] [skip-ref|run] [phase|full] [full]
+# ("phase": k_step phase split; "full": also racecheck/memcheck and smoke())
 cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
 TAG=${1:-run}
 timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/${TAG}_gpu_tests.log 2>&1; echo "exit $?" >> gpurun_out/${TAG}_gpu_tests.log
@@ -22,5 +23,9 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_st
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_render -s 3 -c 1 -o gpurun_out/${TAG}_prof_render python bench.py --config c3 --steps 3 --warmup 3 --no-cpu --secondary "" > /dev/null 2>> gpurun_out/${TAG}_ncu.err
 if [ "$3" == "phase" ]; then
   timeout 600 python tools/phase_timing.py 4096 50 > gpurun_out/${TAG}_phase.txt 2>&1
+fi
+if [ "$3" == "full" ] || [ "$4" == "full" ]; then
+  bash tools/sanitize.sh ${TAG}
+  python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/${TAG}_smoke.txt 2>&1
 fi
 echo done
