@@ -120,3 +120,45 @@ def test_overflow_paths_bit_exact(cuda, caps, obs_mode):
     r = subprocess.run([sys.executable, os.path.join(here, "raster_caps_child.py"), obs_mode],
                        env=dict(os.environ, BS_RENDER_CAPS=caps), capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("near,far", [(0.3, 0.9), (0.01, 0.45)])
+def test_near_far_planes_and_close_ups_bit_exact(cuda, near, far):
+    """Depth-range edge cases: a far plane that cuts through the scene (fragments beyond it are
+    dropped per pixel) and cameras so close that vertices fall behind the near plane or outside
+    the guard band (whole triangles culled) -- every pixel equals the oracle's."""
+    from paper_2410_00425_b200.cameras import CameraConfig, pinhole
+    from paper_2410_00425_b200.tasks import make_task
+
+    w = h = 96
+    N = 8
+    cams = [CameraConfig("cam", pose_p=(0.3, 0.3, 0.3), pose_q=tuple(_look_at_q((0.3, 0.3, 0.3), (0, 0, 0))),
+                         near=near, far=far, **pinhole(w, h, 60.0))]
+    env = make_task("PickCube", N, seed=2, obs_mode="rgbd", cameras=cams)
+    env.step_random(0)
+    g = env.renderer.groups[0]
+    rng = np.random.default_rng(int(far * 1000))
+    views = np.zeros((N, 7))
+    cube = env.scene.actor_pose.cpu().numpy()[:, 0, :3]
+    for e in range(N):  # from just outside the cube to a grazing view along the ground
+        target = cube[e] + rng.uniform(-0.02, 0.02, 3)
+        d = [0.012, 0.02, 0.05, 0.3, 0.6, 1.0, 0.04, 0.25][e]
+        az = rng.uniform(-np.pi, np.pi)
+        eye = target + d * np.array([np.cos(az), np.sin(az), 0.4 if e < 6 else 0.05])
+        eye[2] = max(eye[2], 0.005)
+        views[e, :3], views[e, 3:] = eye, _look_at_q(eye, target)
+    g["pose"].copy_(torch.as_tensor(views[:, None, :], device=g["pose"].device))
+    want = _oracle_frames(env, g, False)
+    env.renderer.render()
+    torch.cuda.synchronize()
+    rgb, depth, seg = g["rgb"].cpu().numpy(), g["depth"].cpu().numpy(), g["seg"].cpu().numpy()
+    clipped = 0
+    for e in range(N):
+        w_rgb, w_depth, w_seg, _, _ = want[e, 0]
+        assert np.array_equal(seg[e, 0].view(np.uint16), w_seg), f"env {e}: seg"
+        assert np.array_equal(depth[e, 0].view(np.uint32), w_depth.view(np.uint32)), f"env {e}: depth"
+        assert np.array_equal(rgb[e, 0], w_rgb), f"env {e}: rgb"
+        hit = w_depth[w_depth > 0]
+        assert hit.size == 0 or (hit.min() >= near and hit.max() <= far)
+        clipped += int((w_depth == 0).sum())
+    assert clipped > 0  # the far plane / near plane actually removed something
