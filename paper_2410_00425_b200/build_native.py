@@ -11,6 +11,8 @@ Usage: ``python -m paper_2410_00425_b200.build_native [--force] [-v]``.
 
 from __future__ import annotations
 
+import hashlib
+import json
 import os
 import shutil
 import subprocess
@@ -48,19 +50,33 @@ def _nvcc() -> str:
     raise RuntimeError("nvcc not found: the batchsim-b200 CUDA library cannot be built")
 
 
-def _deps_mtime() -> float:
-    newest = os.path.getmtime(os.path.join(ROOT, "include", "batchsim_b200.h"))
-    for f in os.listdir(CSRC):
-        if f.endswith((".cuh", ".h")):
-            newest = max(newest, os.path.getmtime(os.path.join(CSRC, f)))
-    return newest
+def _digest(src: str) -> str:
+    """Content hash of one translation unit's inputs: the source, every header it can include
+    and the exact nvcc flags (so a stale object is detected even when file mtimes lie, e.g.
+    after a snapshot copy)."""
+    h = hashlib.sha256()
+    h.update(" ".join(ARCH + COMMON + SOURCES[src]).encode())
+    files = [os.path.join(CSRC, src), os.path.join(ROOT, "include", "batchsim_b200.h")]
+    files += sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
+    for f in files:
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()
+
+
+STAMP = os.path.join(OUT_DIR, "build_stamp.json")
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile every CUDA source for sm_100a and link the shared library; returns its path."""
+    """Compile every CUDA source for sm_100a and link the shared library; returns its path.
+    An object is rebuilt when its content digest (source + headers + flags) changed."""
     nvcc = _nvcc()
     os.makedirs(OUT_DIR, exist_ok=True)
-    hdr_time = _deps_mtime()
+    try:
+        with open(STAMP) as fh:
+            stamp = json.load(fh)
+    except (OSError, ValueError):
+        stamp = {}
     sources = [s for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
     objs = []
     jobs = []
@@ -68,8 +84,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         spath = os.path.join(CSRC, src)
         obj = os.path.join(OUT_DIR, src.replace(".cu", ".o"))
         objs.append(obj)
-        stale = force or not os.path.exists(obj) or os.path.getmtime(obj) < max(
-            os.path.getmtime(spath), hdr_time)
+        digest = _digest(src)
+        stale = force or not os.path.exists(obj) or stamp.get(src) != digest
+        stamp[src] = digest
         if stale:
             cmd = [nvcc, *ARCH, *COMMON, *SOURCES[src], "-c", spath, "-o", obj]
             if verbose:
@@ -87,12 +104,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
         list(ex.map(run, jobs))
-    newest_obj = max(os.path.getmtime(o) for o in objs)
-    if force or jobs or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < newest_obj:
+    link_digest = hashlib.sha256("".join(stamp[s] for s in sources).encode()).hexdigest()
+    if force or jobs or not os.path.exists(LIB_PATH) or stamp.get("__lib__") != link_digest:
         tmp = LIB_PATH + ".tmp"
         cmd = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs]
         run(cmd)
         os.replace(tmp, LIB_PATH)
+    stamp["__lib__"] = link_digest
+    with open(STAMP, "w") as fh:
+        json.dump(stamp, fh, indent=1)
     return LIB_PATH
 
 

@@ -1,0 +1,286 @@
+"""Parity at the BENCHMARKED sizes (BASELINE.json configs C2-C5), GPU product vs the CPU oracle.
+
+Every number bench.py reports comes from one of these configurations, so each is checked here
+at its full env count, not at a 16-env stand-in:
+
+  C2  PickCube-style, state, 4096 envs: every step re-synchronises the oracle to the GPU state
+      and steps both with the same Philox actions.  Contact pair lists (order included),
+      unsupported-pair counters, success/fail/terminated/truncated flags: bit-exact for all
+      4096 envs.  Contact geometry and body/articulation state: |dx| <= 1e-9.  The FK cache
+      (link_pose) against oracle FK of the GPU's own qpos: <= 1e-12.  The state observation
+      against the oracle's obs from the same state: float32, <= 2 ulp-scale (1e-6 abs).
+      Envs start at staggered `elapsed` so truncation + in-kernel auto-reset fire every step.
+  C3  PickCube rgb+depth(+seg) 128x128, 1024 envs: the persistent k_render loops over
+      1024 / 148 ~ 7 frames per CTA; a sample of frames including indices >= 2 x 148 (the 3rd
+      and later frames of a CTA) must equal the oracle rasterizer bit-for-bit.  End to end:
+      frames rendered by the ORACLE from its own FK of the GPU's qpos (state -> FK -> frames,
+      no GPU link_pose) agree with the GPU frames except for a stated pixel bound (FK differs
+      from the oracle in the last ulp, which may move a fixed-point snap on a silhouette).
+  C4  OpenCabinet pointcloud 128x128, 1024 envs, one step re-synchronised; sampled frames:
+      seg bit-exact, pointcloud <= 1e-6 m.
+  C5  PickHetero 2 cameras 256x256, 1024 envs, one step re-synchronised; sampled frames of
+      both cameras bit-exact.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+SEED = 7
+# frames sampled for the render checks: the first / last frames of the first CTAs' first,
+# second, third (>= 2*148) and later persistent-loop iterations, plus random ones
+FRAME_SAMPLE = [0, 1, 147, 148, 149, 295, 296, 297, 443, 444, 591, 740, 888, 1023]
+
+
+def frame_sample(n, extra=10, seed=0):
+    rng = np.random.default_rng(seed)
+    idx = [i for i in FRAME_SAMPLE if i < n] + rng.choice(n, size=min(extra, n), replace=False).tolist()
+    return sorted(set(idx))
+
+
+def gpu_snapshot(env):
+    s = env.scene
+    D = s.models[0].D
+    ap, av = s.actor_pose.cpu().numpy(), s.actor_vel.cpu().numpy()
+    return {"q": s.qpos.cpu().numpy()[:, :D], "qd": s.qvel.cpu().numpy()[:, :D], "ap": ap[:, :, :3],
+            "aq": ap[:, :, 3:], "av": av[:, :, :3], "aw": av[:, :, 3:], "goal": s.goal.cpu().numpy(),
+            "elapsed": s.elapsed.cpu().numpy()}
+
+
+def compare_contacts(env, o_contacts, t):
+    """GPU ContactSet (compacted per env in pair-slot order) vs the oracle's fixed slots, for
+    every env at once: counts and pair ids bit-exact, geometry <= 1e-9."""
+    cnt, pairs, geom = (x.cpu().numpy() for x in env.contacts())
+    N = cnt.shape[0]
+    if not o_contacts:
+        assert (cnt == 0).all()
+        return 0
+    V = np.stack([np.asarray(c[5], bool) for c in o_contacts], 1)  # N x slots
+    assert np.array_equal(cnt, V.sum(1)), f"step {t}: contact counts differ in envs {np.nonzero(cnt != V.sum(1))[0][:8]}"
+    pos = np.cumsum(V, 1) - 1
+    rows = np.arange(N)
+    for s, (i, j, P, n, d, v) in enumerate(o_contacts):
+        e = rows[V[:, s]]
+        if not len(e):
+            continue
+        c = pos[e, s]
+        assert (pairs[e, c, 0] == i).all() and (pairs[e, c, 1] == j).all(), f"step {t}: pair ids at slot {s}"
+        want = np.concatenate([P[e], n[e], d[e][:, None]], 1)
+        err = np.abs(geom[e, c] - want).max()
+        assert err <= 1e-9, f"step {t}: contact geometry err {err:.3e} at slot {s}"
+    return int(V.sum())
+
+
+def assert_close(g, o, atol, what):
+    for k in ("q", "qd", "ap", "aq", "av", "aw", "goal"):
+        err = np.abs(np.asarray(g[k], np.float64) - np.asarray(o[k], np.float64))
+        assert err.max() <= atol, f"{what} {k}: max err {err.max():.3e} at {np.unravel_index(err.argmax(), err.shape)}"
+
+
+# ---------------------------------------------------------------------------------- C2
+def test_c2_4096_envs_step_parity(cuda):
+    from oracle.dynamics import forward_kinematics
+    from oracle.philox import action_uniforms
+    from oracle.tasks import PickCubeOracle
+    from paper_2410_00425_b200 import _native as nat
+    from paper_2410_00425_b200.tasks import make_task, pickcube_scene
+
+    N, STEPS = 4096, 60
+    env = make_task("PickCube", N, seed=SEED)
+    orc = PickCubeOracle(env.spec, pickcube_scene(env.spec), N, SEED)
+    # staggered episode clocks: ~1% of the envs truncate (and auto-reset in the kernel) per step
+    env.scene.elapsed.copy_(torch.arange(N, device=env.device, dtype=torch.int32) % env.spec.max_steps)
+    torch.cuda.synchronize()
+    a = torch.empty((N, env.action_dim), dtype=torch.float32, device=env.device)
+    n_contacts = n_resets = 0
+    for t in range(STEPS):
+        orc.load(gpu_snapshot(env))
+        orc.reset_count[:] = env.scene.reset_count.cpu().numpy().astype(np.uint64)
+        nat.call("bs_random_actions", SEED, t, 0, N, env.action_dim, a.data_ptr(), nat.stream_handle())
+        a_np = action_uniforms(SEED, t, np.arange(N), env.action_dim)
+        assert np.array_equal(a.cpu().numpy().view(np.uint32), a_np.view(np.uint32))
+        r = env.step(a)
+        o_obs, o_rew, o_term, o_trunc, o_info, _ = orc.step(a_np, want_contacts=True)
+        for name, got, want in (("unsupported", r.info["unsupported_pairs"], o_info["unsupported_pairs"]),
+                                ("terminated", r.terminated, o_term), ("truncated", r.truncated, o_trunc),
+                                ("success", r.info["success"], o_info["success"]),
+                                ("fail", r.info["fail"], o_info["fail"])):
+            g = got.cpu().numpy()
+            w = np.asarray(want).astype(g.dtype)
+            assert np.array_equal(g, w), f"step {t}: {name} differs in {int((g != w).sum())} envs"
+        n_resets += int((o_term | o_trunc).sum())
+        n_contacts += compare_contacts(env, o_info["contacts"], t)
+        assert np.abs(r.reward.cpu().numpy() - o_rew).max() <= 1e-5
+        g = gpu_snapshot(env)
+        assert_close(g, orc.snapshot(), 1e-9, f"step {t}")
+        # the FK cache, end to end: oracle FK of the GPU's own joint state
+        LP, LQ = forward_kinematics(orc.model, g["q"])
+        lp = env.scene.link_pose.cpu().numpy()[:, :orc.model.L]
+        assert np.abs(lp[..., :3] - LP).max() <= 1e-12, f"step {t}: link_pose p"
+        assert np.abs(lp[..., 3:] - LQ).max() <= 1e-12, f"step {t}: link_pose q"
+        # the state observation the kernel packed vs the oracle's obs of the same state
+        assert np.abs(r.obs.cpu().numpy() - o_obs).max() <= 1e-6, f"step {t}: state obs"
+    assert n_contacts > 4 * N * STEPS // 2, n_contacts
+    assert n_resets >= STEPS * N // 100, n_resets
+
+
+def test_c2_forward_kinematics_entry_point(cuda):
+    """bs_forward_kinematics (the standalone FK launch) against oracle FK at 4096 envs."""
+    from oracle.dynamics import forward_kinematics
+    from oracle.model import Model
+    from paper_2410_00425_b200.descriptors import pickcube_desc
+    from paper_2410_00425_b200.tasks import make_task
+
+    N = 4096
+    env = make_task("PickCube", N, seed=SEED)
+    rng = np.random.default_rng(0)
+    s = env.scene
+    q = rng.uniform(-2.5, 2.5, (N, s.D_max))
+    s.qpos.copy_(torch.as_tensor(q, device=env.device))
+    s.link_pose.zero_()
+    s.forward_kinematics()
+    torch.cuda.synchronize()
+    m = Model(pickcube_desc(env.spec))
+    LP, LQ = forward_kinematics(m, q[:, :m.D])
+    lp = s.link_pose.cpu().numpy()[:, :m.L]
+    assert np.abs(lp[..., :3] - LP).max() <= 1e-12
+    assert np.abs(lp[..., 3:] - LQ).max() <= 1e-12
+
+
+# ---------------------------------------------------------------------------------- render helpers
+def oracle_frame(env, e, c, model, lp, ap, want_pc=False, colors=None):
+    from oracle import raster
+    from oracle.contacts import shape_world_poses
+
+    R = env.renderer
+    g = R.groups[0]
+    cam = g["cams"][c]
+    L = model.L
+    SP, SQ = shape_world_poses(model, lp[None, :L, :3], lp[None, :L, 3:], ap[None, :model.A, :3],
+                               ap[None, :model.A, 3:])
+    pose, intr = g["pose"][e, c].cpu().numpy(), g["intr"][e, c].cpu().numpy()
+    col = colors if colors is not None else model.s_color[:, :3].astype(np.float32)
+    mi = env.scene.model_index[e]
+    return raster.render_frame(R.mesh.per_model[mi], model.s_seg, SP[0], SQ[0], pose[:3], pose[3:], intr,
+                               cam.width, cam.height, cam.near, cam.far, col, R.light, R.params.ambient,
+                               R.params.diffuse, R.params.background, want_pc)
+
+
+def check_frame(env, e, c, want, what):
+    g = env.renderer.groups[0]
+    rgb, depth, seg = want[0], want[1], want[2]
+    assert np.array_equal(g["seg"][e, c].cpu().numpy().view(np.uint16), seg), f"{what}: seg"
+    assert np.array_equal(g["depth"][e, c].cpu().numpy().view(np.uint32), depth.view(np.uint32)), f"{what}: depth"
+    assert np.array_equal(g["rgb"][e, c].cpu().numpy(), rgb), f"{what}: rgb"
+
+
+# ---------------------------------------------------------------------------------- C3
+def test_c3_1024_frames_persistent_loop_bit_exact(cuda):
+    from oracle.dynamics import forward_kinematics
+    from oracle.model import Model
+    from paper_2410_00425_b200.descriptors import pickcube_desc
+    from paper_2410_00425_b200.tasks import make_task
+
+    N = 1024
+    env = make_task("PickCube", N, seed=SEED, obs_mode="rgbd")
+    for t in range(3):
+        env.step_random(t)
+    torch.cuda.synchronize()
+    model = Model(pickcube_desc(env.spec))
+    lp_all, ap_all = env.scene.link_pose.cpu().numpy(), env.scene.actor_pose.cpu().numpy()
+    q_all = env.scene.qpos.cpu().numpy()[:, :model.D]
+    sample = frame_sample(N)
+    assert max(sample) >= 2 * 148
+    mism = total = 0
+    for e in sample:
+        check_frame(env, e, 0, oracle_frame(env, e, 0, model, lp_all[e], ap_all[e]), f"C3 frame {e}")
+        # end to end: state -> oracle FK -> oracle frames (no GPU link_pose involved)
+        LP, LQ = forward_kinematics(model, q_all[e:e + 1])
+        lp_o = np.concatenate([LP[0], LQ[0]], -1)
+        _, depth, seg, _, _ = oracle_frame(env, e, 0, model, lp_o, ap_all[e])
+        gseg = env.renderer.groups[0]["seg"][e, 0].cpu().numpy().view(np.uint16)
+        mism += int((gseg != seg).sum())
+        total += seg.size
+    # FK agrees to ~1e-16; a pixel can change only where a projected vertex snaps to the other
+    # 1/256-px grid point on a silhouette.  Bound: <= 1e-4 of the sampled pixels.
+    print(f"state->FK->frames: {mism} of {total} sampled seg pixels differ")
+    assert mism <= 1e-4 * total, f"state->frames: {mism} of {total} seg pixels differ"
+
+
+# ---------------------------------------------------------------------------------- C4
+def test_c4_1024_cabinets_step_and_pointcloud(cuda):
+    from oracle.model import Model
+    from oracle.philox import action_uniforms
+    from oracle.tasks import OpenCabinetOracle
+    from paper_2410_00425_b200 import _native as nat
+    from paper_2410_00425_b200.tasks import make_task
+
+    N = 1024
+    env = make_task("OpenCabinet", N, seed=SEED, obs_mode="pointcloud")
+    orc = OpenCabinetOracle(env.spec, env.descs, SEED)
+    a = torch.empty((N, 3), dtype=torch.float32, device=env.device)
+    for t in range(2):
+        s = env.scene
+        orc.load(s.qpos.cpu().numpy(), s.qvel.cpu().numpy())
+        orc.elapsed[:] = s.elapsed.cpu().numpy()
+        orc.reset_count[:] = s.reset_count.cpu().numpy().astype(np.uint64)
+        orc.target[:] = s.target_dof.cpu().numpy()
+        nat.call("bs_random_actions", SEED, t, 0, N, 3, a.data_ptr(), nat.stream_handle())
+        r = env.step(a)
+        o_rew, o_term, o_trunc, o_info, _ = orc.step(action_uniforms(SEED, t, np.arange(N), 3))
+        assert np.array_equal(r.terminated.cpu().numpy().astype(bool), o_term), t
+        assert np.array_equal(r.truncated.cpu().numpy().astype(bool), o_trunc), t
+        assert np.array_equal(r.info["success"].cpu().numpy().astype(bool), o_info["success"]), t
+        snap = orc.snapshot()
+        assert np.abs(s.qpos.cpu().numpy() - snap["q"]).max() <= 1e-9, t
+        assert np.abs(s.qvel.cpu().numpy() - snap["qd"]).max() <= 1e-9, t
+    torch.cuda.synchronize()
+    g = env.renderer.groups[0]
+    lp_all = env.scene.link_pose.cpu().numpy()
+    ap0 = np.zeros((0, 7))
+    for e in frame_sample(N, extra=6):
+        model = Model(env.descs[e])
+        rgb, depth, seg, wpc, _ = oracle_frame(env, e, 0, model, lp_all[e], ap0, want_pc=True)
+        assert np.array_equal(g["seg"][e, 0].cpu().numpy().view(np.uint16), seg), f"C4 frame {e}: seg"
+        assert np.abs(g["pc"][e, 0].cpu().numpy() - wpc).max() <= 1e-6, f"C4 frame {e}: pointcloud"
+
+
+# ---------------------------------------------------------------------------------- C5
+def test_c5_1024_hetero_two_cameras(cuda):
+    from oracle.model import Model
+    from oracle.philox import action_uniforms
+    from oracle.tasks import PickHeteroOracle
+    from paper_2410_00425_b200.tasks import make_task
+
+    N = 1024
+    env = make_task("PickHetero", N, seed=SEED, obs_mode="rgbd")
+    orc = PickHeteroOracle(env.spec, env.descs, SEED)
+
+    def snap():
+        s = env.scene
+        ap, av = s.actor_pose.cpu().numpy(), s.actor_vel.cpu().numpy()
+        return {"q": s.qpos.cpu().numpy()[:, :3], "qd": s.qvel.cpu().numpy()[:, :3], "ap": ap[:, :, :3],
+                "aq": ap[:, :, 3:], "av": av[:, :, :3], "aw": av[:, :, 3:], "goal": s.goal.cpu().numpy(),
+                "elapsed": s.elapsed.cpu().numpy()}
+
+    for t in range(2):
+        orc.load(snap(), env.scene.reset_count.cpu().numpy().astype(np.uint64))
+        r = env.step_random(t)
+        o_rew, o_term, o_trunc, o_info = orc.step(action_uniforms(SEED, t, np.arange(N), 3))
+        assert np.array_equal(r.terminated.cpu().numpy().astype(bool), o_term), t
+        assert np.array_equal(r.truncated.cpu().numpy().astype(bool), o_trunc), t
+        g, o = snap(), orc.snapshot()
+        for k in ("q", "qd", "ap", "aq", "av", "aw"):
+            assert np.abs(g[k] - o[k]).max() <= 1e-9, (t, k)
+    torch.cuda.synchronize()
+    R = env.renderer
+    assert len(R.groups[0]["cams"]) == 2 and R.groups[0]["w"] == 256
+    colors = R.env_color.cpu().numpy()
+    lp_all, ap_all = env.scene.link_pose.cpu().numpy(), env.scene.actor_pose.cpu().numpy()
+    for e in frame_sample(N // 2, extra=4):  # 2 cameras per env: frames 2e, 2e+1
+        model = Model(env.descs[e])
+        for c in range(2):
+            want = oracle_frame(env, e, c, model, lp_all[e], ap_all[e], colors=colors[e, :model.S])
+            check_frame(env, e, c, want, f"C5 env {e} cam {c}")
