@@ -1,15 +1,17 @@
 """Benchmark: env-steps/s of the PickCube-style tabletop task on N B200s, next to the reference
 CPU path timed on the host cores.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2|c3|c4]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config c2|c3|c3_4096|c4|c5] [--secondary c3,c3_4096]
   (N>1: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...)
 
 Workloads (BASELINE.json configs):
 - c2 (the headline, configs[1]): state obs, 4096 envs per GPU;
 - c3 (configs[2]): obs_mode rgb+depth (+seg), one 128x128 camera, 1024 envs per GPU;
-- c4: pointcloud obs from one 128x128 camera, 1024 envs per GPU.
-The default run prints the c2 line and attaches a shorter c3 measurement under
-"secondary".
+- c3_4096: the same sim+render workload at the north star's 4096 envs per GPU;
+- c4 (configs[3]): OpenCabinet, pointcloud obs from one 128x128 camera, 1024 envs per GPU;
+- c5 (configs[4]): PickHetero, 2 jittered 256x256 cameras, 1024 envs per GPU.
+The default run prints the c2 line and attaches c3 and c3_4096 under "secondaries".
 
 One "step" = one env.step over every env on every GPU. That is: controller -> 2 substeps of
 dynamics, contacts and PGS -> FK -> reward/termination -> state obs -> auto-reset, plus the
@@ -20,15 +22,18 @@ Timing rules:
   resident in HBM. The L2 is flushed (a 256 MiB write) BEFORE every timed step, outside the
   events, so every step starts cold. The max is taken over ranks; the figure is whole-job
   env-steps/s.
-- `e2e`: the public API (`Env.step(host action)`). The action is copied from pinned host
-  memory, and obs + reward are copied back every step. Wall clock, synchronised.
+- `e2e`: the public API with host buffers (`Env.step_host(host action)`): actions read from
+  pinned host memory and obs/reward/flags (+ frames) written back every step; wall clock,
+  synchronised, max over ranks.
 - `roofline`: the dominant kernel alone (events around its launch). Algorithmic bytes per
-  env-step / duration, against MEASURED_PEAKS.json hbm_gbs.
+  env-step / duration, against
+  MEASURED_PEAKS.json hbm_gbs.
 - `cpu_baseline` (rank 0, N=1 only): the oracle (CPU restatement of the reference path,
-  numpy) on all host cores, one process per core, for a bounded sample.
+  numpy) on all host cores, one process per core, for a bounded sample (stated, with the CPU
+  model).
 The reference arm (`--impl reference`) times that same CPU path per step on the same
-workload. NCCL is used only after the timed region: the max-over-ranks timing and the rollout
-statistics.
+workload (rank 0 only; every config). NCCL is used only after the timed region: the
+max-over-ranks timing and the rollout statistics.
 """
 
 from __future__ import annotations
@@ -60,6 +65,9 @@ WORKLOADS = {
            "desc": "C2 PickCube-style (ARM3 + cube + ground), obs_mode=state, 4096 envs/GPU"},
     "c3": {"task": "PickCube", "envs": 1024, "obs_mode": "rgbd",
            "desc": "C3 PickCube-style, obs_mode=rgb+depth (+seg) 1 camera 128x128, 1024 envs/GPU"},
+    "c3_4096": {"task": "PickCube", "envs": 4096, "obs_mode": "rgbd",
+                "desc": "C3 at the north-star scale: PickCube-style sim+render, rgb+depth (+seg) 1 camera "
+                        "128x128, 4096 envs/GPU"},
     "c4": {"task": "OpenCabinet", "envs": 1024, "obs_mode": "pointcloud",
            "desc": "C4 OpenCabinet (ARM3 + per-env 2-6 drawer/door cabinet), obs_mode=pointcloud 1 camera "
                    "128x128, 1024 envs/GPU"},
@@ -145,25 +153,31 @@ def _traffic(kernel: str, workload: str):
 
 
 def sim_bytes_per_env_step(scene, obs_dim, action_dim):
-    """Bytes the fused step must move per env-step.
-
-    Counted: the action read; articulation and actor state read and written; the drive-target
-    write; goal read/write; obs and reward writes; flags and counters. Scratch (link poses,
-    contact rows) is on-chip; the link-pose cache write counts as output."""
+    """Algorithmic bytes of one env-step on SURVEY.md section 8(d)'s basis:
+    the action read; articulation (qpos, qvel) and actor (pose 7 + vel 6) state read + write;
+    the goal read; the state obs + reward written; the four flag bytes; elapsed read + write.
+    fp64 state (the reference's sim precision).  Intermediates the engine also writes -- the
+    link-pose (FK) cache, drive targets, counters -- are NOT algorithmic: reported separately
+    by aux_bytes_per_env_step."""
     D = max(m.D for m in scene.models)
     A = max(m.A for m in scene.models)
-    L = max(m.L for m in scene.models)
     f8 = 8
     b = 4 * action_dim                       # action (f32)
     b += 2 * 2 * D * f8                      # qpos, qvel read + write
-    b += D * f8                              # drive targets write
     b += 2 * A * 13 * f8                     # actor pose (7) + vel (6) read + write
-    b += 2 * 3 * f8                          # goal read + write
-    b += L * 7 * f8                          # link-pose cache write
+    b += 3 * f8                              # goal read
     b += 4 * obs_dim + 4                     # state obs + reward (f32)
-    b += 4 + 4                               # terminated/truncated/success/fail (u8) + unsupported (i32)
-    b += 2 * (4 + 4 + 1) + 4 + 4             # elapsed, reset_count, diverged r/w; model_id, target_dof
+    b += 4                                   # terminated / truncated / success / fail (u8)
+    b += 2 * 4                               # elapsed read + write
     return b
+
+
+def aux_bytes_per_env_step(scene):
+    """Non-algorithmic bytes the fused step also moves: the link-pose cache write, drive
+    targets, goal write-back, reset/divergence counters, unsupported-pair count, model/target ids."""
+    D = max(m.D for m in scene.models)
+    L = max(m.L for m in scene.models)
+    return L * 7 * 8 + D * 8 + 3 * 8 + 2 * (4 + 1) + 4 + 4 + 4
 
 
 def render_bytes_per_env_step(renderer, scene):
@@ -180,49 +194,129 @@ def render_bytes_per_env_step(renderer, scene):
 
 
 # ------------------------------------------------------------------------------ CPU path
-def _cpu_worker(args):
-    """One host process: the oracle (numpy restatement of the reference path) on a slice of
-    envs.  Runs `warmup` steps, waits on the barrier, then `steps` steps (or `seconds`)."""
-    (rank, n_envs, env_offset, seed, warmup, steps, seconds, obs_mode, barrier, q) = args
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    os.environ["OMP_NUM_THREADS"] = "1"
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
+def _cpu_task(name, n_envs, env_offset, total_envs, seed):
+    """The CPU restatement of workload `name` (oracle/: numpy, fp64 dynamics, fp32 raster) for
+    the global envs [env_offset, env_offset + n_envs) of a `total_envs` batch.  Returns
+    step(k): one env.step of those envs with the k-th Philox action draw, plus their frames."""
     import numpy as np
 
+    from oracle import raster
+    from oracle.contacts import shape_world_poses
+    from oracle.dynamics import forward_kinematics
+    from oracle.model import BODY_ACTOR, Model
     from oracle.philox import action_uniforms
-    from oracle.tasks import PickCubeOracle
-    from paper_2410_00425_b200.descriptors import pickcube_desc, PickCubeSpec
+    from paper_2410_00425_b200 import descriptors as Dd
+    from paper_2410_00425_b200 import meshes
+    from paper_2410_00425_b200.cameras import (CameraConfig, CameraJitter, RenderParams, default_cameras,
+                                               look_at, pinhole, randomize_cameras)
+    from paper_2410_00425_b200.scene import PackedModel
 
-    spec = PickCubeSpec()
-    orc = PickCubeOracle(spec, pickcube_desc(spec), n_envs, seed, env_offset=env_offset)
+    wl = WORKLOADS[name]
     ids = np.arange(env_offset, env_offset + n_envs)
-    render = None
-    if obs_mode != "state":
-        from oracle import raster
-        from oracle.contacts import shape_world_poses
-        from paper_2410_00425_b200 import meshes
-        from paper_2410_00425_b200.cameras import RenderParams, default_cameras
+    rp = RenderParams()
+    light = np.asarray(rp.light_dir, np.float64) / np.linalg.norm(rp.light_dir)
+    pc = wl["obs_mode"] == "pointcloud"
+    if wl["task"] == "PickCube":
+        spec = Dd.PickCubeSpec()
+        from oracle.tasks import PickCubeOracle
 
-        m = orc.model
-        kinds = {0: "sphere", 1: "box", 2: "capsule", 3: "cylinder", 4: "plane"}
-        mesh = meshes.model_mesh([{"kind": kinds[int(m.s_kind[s])], "size": tuple(m.s_size[s])} for s in range(m.S)])
-        cam = default_cameras()[0]
-        rp = RenderParams()
-        L = np.asarray(rp.light_dir) / np.linalg.norm(rp.light_dir)
-        colors = m.s_color[:, :3].astype(np.float32)
+        orc = PickCubeOracle(spec, Dd.pickcube_desc(spec), n_envs, seed, env_offset=env_offset)
+        descs = [Dd.pickcube_desc(spec)] * n_envs
+        cams, jitter = default_cameras(), CameraJitter()
+
+        def poses():  # (env -> (model, LP, LQ, AP, AQ))
+            LP, LQ = orc.link_poses()
+            return [(0, LP[e], LQ[e], orc.st.ap[e], orc.st.aq[e]) for e in range(n_envs)]
+    elif wl["task"] == "OpenCabinet":
+        from oracle.tasks import OpenCabinetOracle
+
+        spec = Dd.OpenCabinetSpec()
+        descs = Dd.opencabinet_descs(spec, total_envs, seed)[env_offset:env_offset + n_envs]
+        orc = OpenCabinetOracle(spec, descs, seed, env_offset=env_offset)
+        cams, jitter = default_cameras(), CameraJitter()
+
+        def poses():
+            out = [None] * n_envs
+            for g in orc.groups:
+                LP, LQ = forward_kinematics(g["model"], g["st"].q)
+                for r, e in enumerate(g["idx"]):
+                    out[e] = (e, LP[r], LQ[r], np.zeros((0, 3)), np.zeros((0, 4)))
+            return out
+    else:  # PickHetero
+        from oracle.tasks import PickHeteroOracle
+
+        spec = Dd.PickHeteroSpec()
+        descs = Dd.hetero_descs(spec, total_envs, seed)[env_offset:env_offset + n_envs]
+        orc = PickHeteroOracle(spec, descs, seed, env_offset=env_offset)
+        res = spec.camera_res
+        cams = [CameraConfig(n, pose_p=eye, pose_q=look_at(eye, (-0.15, 0.0, 0.02)), **pinhole(res, res, 60.0))
+                for n, eye in (("base_camera", (0.15, 0.5, 0.4)), ("side_camera", (0.15, -0.5, 0.4)))]
+        jitter = CameraJitter(spec.camera_pos_jitter, spec.camera_rot_jitter, 0.0)
+
+        def poses():
+            out = [None] * n_envs
+            for idx, o in orc.groups:
+                LP, LQ = o.link_poses()
+                for r, e in enumerate(idx):
+                    out[e] = (e, LP[r], LQ[r], o.st.ap[r], o.st.aq[r])
+            return out
+    render = None
+    if wl["obs_mode"] != "state":
+        models = [Model(d) for d in descs] if wl["task"] != "PickCube" else [Model(descs[0])]
+        control = spec.control()
+        mesh_cache = {}
+
+        def mesh_of(e):
+            d = descs[e]
+            k = d.key() if hasattr(d, "key") else 0
+            if k not in mesh_cache:
+                mesh_cache[k] = meshes.model_mesh(PackedModel(d, control).shapes)
+            return mesh_cache[k]
+        cpose, cintr = randomize_cameras(cams, n_envs, seed, jitter, env_offset)
+        colors = [m.s_color[:, :3].astype(np.float32).copy() for m in models]
+        if wl["task"] == "PickHetero":
+            objs = Dd.hetero_objects(spec, total_envs, seed)[env_offset:env_offset + n_envs]
+            for e, (_, _, rgb) in enumerate(objs):
+                m = models[e]
+                colors[e][[s for s in range(m.S) if m.s_btype[s] == BODY_ACTOR]] = rgb  # the actor's shape
 
         def render():
-            LP, LQ = orc.link_poses()
-            SP, SQ = shape_world_poses(m, LP, LQ, orc.st.ap, orc.st.aq)
-            for e in range(n_envs):
-                raster.render_frame(mesh, m.s_seg, SP[e], SQ[e], np.asarray(cam.pose_p), np.asarray(cam.pose_q),
-                                    (cam.fx, cam.fy, cam.cx, cam.cy), cam.width, cam.height, cam.near, cam.far,
-                                    colors, L, rp.ambient, rp.diffuse, rp.background, obs_mode == "pointcloud")
+            for (mi, LP, LQ, AP, AQ), e in zip(poses(), range(n_envs)):
+                m = models[mi]
+                SP, SQ = shape_world_poses(m, LP[None], LQ[None], AP[None], AQ[None])
+                for c, cam in enumerate(cams):
+                    raster.render_frame(mesh_of(e), m.s_seg, SP[0], SQ[0], cpose[e, c, :3], cpose[e, c, 3:],
+                                        cintr[e, c], cam.width, cam.height, cam.near, cam.far, colors[mi], light,
+                                        rp.ambient, rp.diffuse, rp.background, pc)
+    adim = 3
 
-    def one(k):
-        orc.step(action_uniforms(seed, k, ids, 3))
+    def step(k):
+        orc.step(action_uniforms(seed, k, ids, adim))
         if render is not None:
             render()
+    return step
 
+
+def _cpu_worker(args):
+    """One host process: the CPU path on a slice of envs.  Runs `warmup` steps, waits on the
+    barrier, then `steps` steps (or `seconds`)."""
+    (rank, name, n_envs, env_offset, total_envs, seed, warmup, steps, seconds, barrier, q) = args
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    os.environ["OMP_NUM_THREADS"] = "1"
+    one = _cpu_task(name, n_envs, env_offset, total_envs, seed)
     for k in range(warmup):
         one(k)
     barrier.wait()
@@ -238,55 +332,68 @@ def _cpu_worker(args):
     q.put((rank, k, n_envs, time.perf_counter() - t0))
 
 
-def cpu_reference(total_envs, warmup, steps=None, seconds=None, seed=0, obs_mode="state"):
-    """Time the CPU path with one process per host core.  Returns (env-steps/s, cores, info)."""
+def cpu_reference(name, sample_envs, total_envs, warmup, steps=None, seconds=None, seed=0):
+    """Time the CPU path of workload `name` with one process per host core on the global envs
+    [0, sample_envs) of a `total_envs` batch.  Returns (env-steps/s, cores, info)."""
     import multiprocessing as mp
 
     cores = len(os.sched_getaffinity(0))
-    procs = max(1, min(cores, total_envs))
+    procs = max(1, min(cores, sample_envs))
     ctx = mp.get_context("spawn")
     barrier = ctx.Barrier(procs)
     q = ctx.Queue()
-    per = [total_envs // procs + (1 if r < total_envs % procs else 0) for r in range(procs)]
+    per = [sample_envs // procs + (1 if r < sample_envs % procs else 0) for r in range(procs)]
     offs = [sum(per[:r]) for r in range(procs)]
     ps = [ctx.Process(target=_cpu_worker,
-                      args=((r, per[r], offs[r], seed, warmup, steps, seconds, obs_mode, barrier, q),))
+                      args=((r, name, per[r], offs[r], total_envs, seed, warmup, steps, seconds, barrier, q),))
           for r in range(procs)]
     for p in ps:
         p.start()
     res = [q.get() for _ in ps]
     for p in ps:
         p.join()
+    what = (f"all {total_envs} envs" if sample_envs == total_envs else
+            f"a sample of {sample_envs} of the workload's {total_envs} envs (global envs 0-{sample_envs - 1})")
     if steps is not None:
         t = max(r[3] for r in res)
-        rate = total_envs * steps / t
-        info = f"{procs} procs x ~{per[0]} envs, {steps} steps of all {total_envs} envs, {t:.1f} s"
+        rate = sample_envs * steps / t
+        info = f"{procs} procs x ~{per[0]} envs: {steps} steps of {what}, {t:.1f} s"
     else:
         rate = sum(r[1] * r[2] / r[3] for r in res)
-        info = (f"{procs} procs x ~{per[0]} envs ({total_envs} envs total), "
-                f"{min(r[1] for r in res)}-{max(r[1] for r in res)} steps each, ~{seconds:.0f} s")
-    return rate, procs, info
+        info = (f"{procs} procs x ~{per[0]} envs: {min(r[1] for r in res)}-{max(r[1] for r in res)} steps of "
+                f"{what}, ~{seconds:.0f} s")
+    return rate, procs, info + f"; CPU: {cpu_model()}"
+
+
+def cpu_sample_envs(name, total_envs):
+    """Bounded CPU sample: every env for state-only workloads; 4 envs per host core for the
+    rendering ones (a step over all of them would take tens of seconds)."""
+    if WORKLOADS[name]["obs_mode"] == "state":
+        return total_envs
+    return min(total_envs, 4 * len(os.sched_getaffinity(0)))
+
+
+def config_for(name, world):
+    """The `config` dict of a workload: identical in both arms (the driver compares them)."""
+    wl = WORKLOADS[name]
+    return {"workload": wl["desc"], "num_envs_per_gpu": wl["envs"], "global_envs": wl["envs"] * world,
+            "obs_mode": wl["obs_mode"], "sim_freq": 120, "control_freq": 60, "solver_pos_iters": 4,
+            "solver_vel_iters": 0, "parallelism": f"env-shard x{world}",
+            "l2": "flushed (256 MiB write) before each timed GPU step; inputs resident"}
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    wl = WORKLOADS[args.config]
-    if wl["task"] != "PickCube":
-        print(json.dumps({"impl": "reference", "unavailable": f"CPU reference arm implemented for PickCube "
-                          f"workloads (c2, c3); {args.config} is {wl['task']}"}), flush=True)
-        return 0
-    total = wl["envs"] * args.gpus
-    rate, cores, info = cpu_reference(total, args.warmup, steps=args.steps, seed=args.seed, obs_mode=wl["obs_mode"])
+    total = WORKLOADS[args.config]["envs"] * args.gpus
+    sample = cpu_sample_envs(args.config, total)
+    rate, cores, info = cpu_reference(args.config, sample, total, args.warmup, steps=args.steps, seed=args.seed)
     ms = total / rate * 1e3
     line = {"metric": METRIC, "value": rate, "unit": "env-steps/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (Philox-seeded resets and actions)",
-            "impl": "reference",
-            "config": {"workload": wl["desc"].replace(f"{wl['envs']} envs/GPU", f"{total} envs"),
-                       "num_envs": total, "sim_freq": 120, "control_freq": 60, "solver_pos_iters": 4,
-                       "solver_vel_iters": 0},
+            "impl": "reference", "config": config_for(args.config, args.gpus),
             "cpu_baseline": {"value": rate, "unit": "env-steps/s", "cores": cores, "kind": "port",
                              "sample": info},
             "e2e": {"value": rate, "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -295,17 +402,9 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------------------ GPU path
-def _allreduce(dist, t, op):
-    """All-reduce in place; through host memory when the backend cannot reduce CUDA tensors."""
-    if dist.get_backend() == "nccl":
-        dist.all_reduce(t, op=op)
-    else:
-        h = t.cpu()
-        dist.all_reduce(h, op=op)
-        t.copy_(h)
-
-
 def measure(env, steps, warmup, flush, dist, local, seed_step=0):
+    from paper_2410_00425_b200 import dist as bdist
+
     """Device timing of `steps` env steps: the steps' synthetic actions are generated into HBM
     before the timed region (Philox, the same stream step_random uses); per step, flush L2
     (untimed), then events around the fused step and the render."""
@@ -338,8 +437,7 @@ def measure(env, steps, warmup, flush, dist, local, seed_step=0):
     torch.cuda.synchronize()
     t = torch.tensor([sum(e[0].elapsed_time(e[3]) for e in ev), sum(e[1].elapsed_time(e[2]) for e in ev),
                       sum(e[2].elapsed_time(e[3]) for e in ev)], dtype=torch.float64, device=env.device)
-    if dist is not None:
-        _allreduce(dist, t, dist.ReduceOp.MAX)
+    bdist.max_over_ranks(t)  # the job is as slow as its slowest rank
     # k_step, and per camera group k_frame_setup + k_render
     launches = 1 + (2 * len(env.renderer.groups) if env.renderer is not None else 0)
     return {"step_ms": float(t[0]), "sim_ms": float(t[1]), "render_ms": float(t[2]), "clocks": clk.summary(),
@@ -347,6 +445,8 @@ def measure(env, steps, warmup, flush, dist, local, seed_step=0):
 
 
 def measure_e2e(env, steps, dist, seed):
+    from paper_2410_00425_b200 import dist as bdist
+
     """The public API with host buffers: Env.step_host(host action) -- one CUDA graph in which
     the step kernel reads the pinned host actions and writes obs / reward / flags to pinned host
     memory over PCIe (zero-copy), plus the render and the D2H copies of the frames -- then a
@@ -370,9 +470,7 @@ def measure_e2e(env, steps, dist, seed):
         _ = out["reward"]
     e2e_s = time.perf_counter() - t0
     if dist is not None:
-        tt = torch.tensor([e2e_s], dtype=torch.float64, device=env.device)
-        _allreduce(dist, tt, dist.ReduceOp.MAX)
-        e2e_s = float(tt[0])
+        e2e_s = float(bdist.max_over_ranks(torch.tensor([e2e_s], dtype=torch.float64, device=env.device))[0])
     return e2e_s, h2d, d2h
 
 
@@ -389,6 +487,8 @@ def _flatten(d, prefix=""):
 def run_workload(name, steps, warmup, world, rank, local, dist, flush, seed, e2e_steps, cpu):
     import torch
 
+    from paper_2410_00425_b200 import dist as bdist
+
     from paper_2410_00425_b200.tasks import make_task
 
     wl = WORKLOADS[name]
@@ -399,8 +499,7 @@ def run_workload(name, steps, warmup, world, rank, local, dist, flush, seed, e2e
     m = measure(env, steps, warmup, flush, dist, local)
     value = n_global * steps / (m["step_ms"] / 1e3)
     stats = torch.stack([env.success.sum().double(), env.terminated.sum().double(), env.truncated.sum().double()])
-    if dist is not None:
-        _allreduce(dist, stats, dist.ReduceOp.SUM)  # rollout statistics: the only data collective
+    bdist.reduce_stats(stats)  # rollout statistics: the only data collective
     e2e_s, h2d, d2h = measure_e2e(env, e2e_steps, dist, seed + rank)
     e2e = {"value": n_global * e2e_steps / e2e_s, "unit": "env-steps/s", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h, "steps": e2e_steps,
@@ -411,7 +510,8 @@ def run_workload(name, steps, warmup, world, rank, local, dist, flush, seed, e2e
     sim_b = sim_bytes_per_env_step(env.scene, env.obs_dim, env.action_dim)
     sim_s = m["sim_ms"] / 1e3 / steps
     kernels = {"k_step": {"us_per_launch": sim_s * 1e6, "bytes_per_env_step": sim_b,
-                          "achieved_gbs": sim_b * N / sim_s / 1e9}}
+                          "achieved_gbs": sim_b * N / sim_s / 1e9,
+                          "aux_bytes_per_env_step": aux_bytes_per_env_step(env.scene)}}
     dominant = "k_step"
     if env.renderer is not None:
         rb = render_bytes_per_env_step(env.renderer, env.scene)
@@ -428,10 +528,7 @@ def run_workload(name, steps, warmup, world, rank, local, dist, flush, seed, e2e
             "warmup": warmup, "ms_per_step": m["step_ms"] / steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (Philox-seeded resets; device-generated uniform actions, resident in HBM before the timed region)",
-            "config": {"workload": wl["desc"], "num_envs_per_gpu": wl["envs"], "global_envs": n_global,
-                       "obs_mode": wl["obs_mode"], "sim_freq": 120, "control_freq": 60, "solver_pos_iters": 4,
-                       "solver_vel_iters": 0, "parallelism": f"env-shard x{world}",
-                       "l2": "flushed (256 MiB write) before each timed step"},
+            "config": config_for(name, world),
             "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": m["clocks"],
             "gpu_launches": m["launches"],
             "rollout_stats": {"success": float(stats[0]), "terminated": float(stats[1]), "truncated": float(stats[2])}}
@@ -448,19 +545,17 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world == 1 and args.gpus > 1:
         raise SystemExit("--gpus N>1 must be launched with torch.distributed.run (one rank per GPU)")
-    # CPU baselines first (before CUDA is initialised in this process; spawn-based workers)
-    cpu, cpu2 = None, None
-    if rank == 0 and world == 1 and not args.no_cpu and WORKLOADS[args.config]["task"] == "PickCube":
-        wl = WORKLOADS[args.config]
-        rate, cores, info = cpu_reference(wl["envs"], 2, seconds=args.cpu_seconds, seed=args.seed,
-                                          obs_mode=wl["obs_mode"])
-        cpu = {"value": rate, "unit": "env-steps/s", "cores": cores, "kind": "port", "sample": info}
-        if args.secondary and WORKLOADS[args.secondary]["task"] == "PickCube":
-            w2 = WORKLOADS[args.secondary]
-            n2 = 4 * len(os.sched_getaffinity(0))  # bounded sample: 4 envs per core
-            rate, cores, info = cpu_reference(n2, 1, seconds=args.cpu_seconds / 2, seed=args.seed,
-                                              obs_mode=w2["obs_mode"])
-            cpu2 = {"value": rate, "unit": "env-steps/s", "cores": cores, "kind": "port", "sample": info}
+    # CPU baselines first (before CUDA is initialised in this process; spawn-based workers):
+    # rank 0 at N=1 only, a bounded sample of each workload (cpu_sample_envs)
+    secondaries = [w for w in (args.secondary or "").split(",") if w and w != args.config]
+    cpus = {}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        for k, name in enumerate([args.config] + secondaries):
+            total = WORKLOADS[name]["envs"]
+            rate, cores, info = cpu_reference(name, cpu_sample_envs(name, total), total, 1 if k else 2,
+                                              seconds=args.cpu_seconds if k == 0 else args.cpu_seconds / 2,
+                                              seed=args.seed)
+            cpus[name] = {"value": rate, "unit": "env-steps/s", "cores": cores, "kind": "port", "sample": info}
 
     local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
@@ -474,16 +569,22 @@ def run_ours(args):
         else:
             dist.init_process_group(backend)
     from paper_2410_00425_b200 import _native as nat
+    from paper_2410_00425_b200 import dist as bdist
 
     nat.ensure_device(local)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=torch.device("cuda", local))
     line = run_workload(args.config, args.steps, args.warmup, world, rank, local, dist, flush, args.seed,
-                        max(args.steps, 20), cpu)
-    if args.secondary:
-        sec = run_workload(args.secondary, max(args.steps // 4, 20), max(args.warmup, 3), world, rank, local, dist,
-                           flush, args.seed, 20, cpu2)
-        line["secondary"] = {k: sec[k] for k in ("value", "unit", "ms_per_step", "steps", "config", "e2e", "roofline",
-                                                 "cpu_baseline", "clocks", "gpu_launches")}
+                        max(args.steps, 20), cpus.get(args.config))
+    line["communicator"] = bdist.describe()
+    secs = []
+    for name in secondaries:
+        sec = run_workload(name, max(args.steps // 4, 20), max(args.warmup, 3), world, rank, local, dist,
+                           flush, args.seed, 20, cpus.get(name))
+        secs.append({k: sec[k] for k in ("value", "unit", "ms_per_step", "steps", "config", "e2e", "roofline",
+                                         "cpu_baseline", "clocks", "gpu_launches")})
+    if secs:
+        line["secondary"] = secs[0]          # the first extra workload (kept for older readers)
+        line["secondaries"] = secs
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
@@ -498,7 +599,8 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", choices=sorted(WORKLOADS), default="c2")
-    ap.add_argument("--secondary", default="c3", help="extra workload measured after the headline ('' = none)")
+    ap.add_argument("--secondary", default="c3,c3_4096",
+                    help="comma list of extra workloads measured after the headline ('' = none)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline legs")
@@ -506,8 +608,6 @@ def main(argv=None):
     args = ap.parse_args(argv)
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
-    if args.secondary == args.config:
-        args.secondary = ""
     if args.envs:
         WORKLOADS[args.config] = dict(WORKLOADS[args.config], envs=args.envs,
                                       desc=WORKLOADS[args.config]["desc"] + f" [override: {args.envs} envs/GPU]")

@@ -34,7 +34,7 @@ extern "C" {
 #define BS_ERR_UNSUPPORTED 6 /* ModelError      (errors.py:40) */
 
 /* ABI version: bumped whenever a signature or a struct layout below changes. */
-#define BS_ABI_VERSION 7
+#define BS_ABI_VERSION 8
 int bs_abi_version(void);
 
 /* Bind the library's CUDA runtime to `device` (call once per process/thread before use;
@@ -80,6 +80,34 @@ int bs_pose_to_matrix_f64(const double* p, const double* q, int64_t n, double* m
  * scalar, must be zeroed by the caller); the caller raises when it exceeds 1e-6. */
 int bs_pose_from_matrix_f64(const double* m, int64_t n, double* p_out, double* q_out,
                             double* err_out, void* stream);
+
+/* Quaternion algebra (pose.py:43-88 quat_mul / quat_conjugate / quat_rotate / quat_to_matrix,
+ * pose.py:91-122 matrix_to_quat).  Binary ops broadcast a singleton side (na == nb, or either
+ * is 1; else BS_ERR_DIMENSION, like pose.py:167-174).  fp64 results are bit-identical to
+ * numpy's (separately rounded + and *, the reference's operation order). */
+int bs_quat_mul_f64(const double* a, int64_t na, const double* b, int64_t nb, double* out,
+                    void* stream);
+int bs_quat_mul_f32(const float* a, int64_t na, const float* b, int64_t nb, float* out,
+                    void* stream);
+int bs_quat_conjugate_f64(const double* q, int64_t n, double* out, void* stream);
+int bs_quat_rotate_f64(const double* q, int64_t nq, const double* v, int64_t nv, double* out,
+                       void* stream);
+int bs_quat_rotate_f32(const float* q, int64_t nq, const float* v, int64_t nv, float* out,
+                       void* stream);
+/* q: [n][4] -> m: [n][3][3] row-major. */
+int bs_quat_to_matrix_f64(const double* q, int64_t n, double* m_out, void* stream);
+/* m: [n][3][3] -> q: [n][4], Shepperd's method (branch = first argmax of trace, m00, m11, m22),
+ * normalized once. */
+int bs_matrix_to_quat_f64(const double* m, int64_t n, double* q_out, void* stream);
+
+/* TransformMatrixBatch (pose.py:125-164) on [n][4][4] row-major fp64 matrices: compose
+ * (= matmul, singleton broadcast), rigid inverse (R^T, -R^T t), transform_points (R x + t for
+ * [np][k][3] points, singleton broadcast on either side). */
+int bs_tmat_compose_f64(const double* a, int64_t na, const double* b, int64_t nb, double* out,
+                        void* stream);
+int bs_tmat_inverse_f64(const double* m, int64_t n, double* out, void* stream);
+int bs_tmat_transform_points_f64(const double* m, int64_t n, const double* pts, int64_t np_,
+                                 int64_t k, double* out, void* stream);
 
 /* ------------------------------------------------------ scene store (SoA) ---- */
 /* The SoA GPU state store that replaces the reference's per-env SceneBatch objects
@@ -177,6 +205,8 @@ typedef struct BsStepOutputs {
   double* ep_return_out;       /* [N] its return (sum of the step rewards)         */
   int32_t* ep_length_out;      /* [N] its length in steps                          */
   uint8_t* ep_flags_out;       /* [N] bit0 success_once bit1 success_at_end bit2 fail_once bit3 fail_at_end */
+  float* final_obs;            /* [N][obs_dim] state obs of the state an episode ended in, written only for
+                                  envs auto-reset this step (may be NULL; ABI 8) */
 } BsStepOutputs;
 
 typedef struct BsSimParams {
@@ -197,6 +227,7 @@ typedef struct BsSimParams {
   int32_t early_termination;   /* 1: terminated = success | fail                 */
   uint64_t seed;
   double task_f[16];           /* task constants (documented per task in DESIGN.md) */
+  double control_freq;         /* Hz: delta controllers' target velocity = delta * control_freq (ABI 8) */
 } BsSimParams;
 
 /* One control step for every env: controller -> substeps x (drives + dynamics +

@@ -3,8 +3,14 @@ integration, limits, divergence) -> FK cache.  Test infrastructure (oracle/__ini
 
 Vectorised over a batch of B envs that share one Model.  Follows SPEC.md:319-327 (step),
 SPEC.md:346-354 (PGS), SPEC.md:402-410 (controllers) with DESIGN.md's decisions:
-  A-16  implicit PD drives: (M + dt*(kd+damping) + dt^2*kp) qdd = clamp(kp(q*-q-dt*qd) -
-        kd*qd, +-limit) - damping*qd - C(q, qd)   (stable at kp=1000 and dt=1/120)
+  A-16  PD drives with a target position AND a target velocity (DriveTargets):
+        tau = kp(q* - q) + kd(qd* - qd), the gains taken "per unit inertia scale"
+        (SPEC.md:427): Kp = kp * m, Kd = kd * m with m = M_ii(q) the joint-space inertia of the
+        dof, so kd = 2 sqrt(kp) is critical damping for every dof whatever its inertia.  The
+        drive is evaluated implicitly at the end-of-substep velocity (stable at kp = 1000,
+        dt = 1/120):
+          (M + diag(dt*(Kd + damping) + dt^2*Kp)) qdd
+              = clamp(Kp(q* - q - dt*qd) + Kd(qd* - qd), +-limit) - damping*qd - C(q, qd)
   A-7   joint limits: clamp after integration, zero the velocity into the limit
   A-8   free bodies: explicit gyroscopic term, q <- normalize(q + dt/2 (0,w) q)
   bias  normal-row target: beta*(d-slop)/dt if d > slop; 0 if 0 <= d <= slop; d/dt if d < 0
@@ -53,6 +59,7 @@ class Drives:
     kd: np.ndarray
     force_limit: np.ndarray
     target: np.ndarray = None
+    target_vel: np.ndarray = None
 
 
 @dataclass
@@ -93,9 +100,12 @@ def substep(model, st: State, drv: Drives, cfg: SimConfig, want_contacts=False):
     if D:
         C = rnea_bias(model, S, V, inert, qd, g)
         M = crba(model, S, inert)
-        arm = dt * (drv.kd + model.damping) + (dt * dt) * drv.kp
-        Mt = M + arm[None, :] * np.eye(D)[None]
-        tau = np.clip(drv.kp * ((drv.target - q) - dt * qd) + drv.kd * (0.0 - qd),
+        m_ii = np.diagonal(M, axis1=1, axis2=2)           # inertia scale of each dof (A-16)
+        Kp, Kd = drv.kp * m_ii, drv.kd * m_ii
+        tv = np.zeros_like(q) if drv.target_vel is None else drv.target_vel
+        arm = dt * (Kd + model.damping) + (dt * dt) * Kp
+        Mt = M + arm[:, :, None] * np.eye(D)[None]
+        tau = np.clip(Kp * ((drv.target - q) - dt * qd) + Kd * (tv - qd),
                       -drv.force_limit, drv.force_limit) - model.damping * qd
         qdd = np.linalg.solve(Mt, (tau - C)[..., None])[..., 0]
         Mt_inv = np.linalg.inv(Mt)
@@ -216,18 +226,32 @@ def crba_rnea_qdd(model, q, qd, tau, gravity):
 PD_JOINT_POS, PD_JOINT_DELTA_POS, PD_EE_DELTA_POSE = "pd_joint_pos", "pd_joint_delta_pos", "pd_ee_delta_pose"
 
 
-def controller_targets(model, ctrl, q, action):
-    """SPEC.md:402-410.  ctrl: mode, dofs (controlled dof indices), scale; returns (B, D)
-    targets (uncontrolled dofs keep target = current q, with kp = 0 they are undriven).
-    pd_ee_delta_pose: twist = (a[0:3] * scale m, a[3:6] * rot_scale rad),
-    world frame, at the ee link origin; dq = J^T (J J^T + lam^2 I)^-1 twist over the controlled
-    columns of the geometric Jacobian; target = clamp(q + dq)."""
+def controller_targets(model, ctrl, q, action, control_freq=60):
+    """SPEC.md:402-410 -> DriveTargets: (B, D) target positions and velocities.
+    ctrl: mode, dofs (controlled dof indices), scale.  Uncontrolled dofs keep target = current q
+    and target velocity 0 (with kp = kd = 0 they are undriven).
+
+    pd_joint_pos        target = unnormalize(a) clamped; target velocity 0.
+    pd_joint_delta_pos  target = clamp(q + a * scale); the delta is a motion over one control
+                        period, so target velocity = (target - q) * control_freq.
+    pd_ee_delta_pose twist = (a[0:3] * scale m in the world
+                        frame, R_ee (a[3:6] * rot_scale) -- the axis-angle is given in the EE
+                        frame and rotated to the world), at the ee link origin;
+                        dq = J^T (J J^T + lam^2 I)^-1 twist over the controlled columns of the
+                        geometric Jacobian; target = clamp(q + dq), velocity as for the joint
+                        delta.
+    base_forward_rotate velocity targets on the abstract base joints
+                        (controlled dofs 0, 1, 2 = x, y, yaw): (a0 * scale cos yaw,
+                        a0 * scale sin yaw, a1 * rot_scale) m/s, m/s, rad/s; position targets
+                        stay at q (the base dofs carry kp = 0: a pure velocity servo)."""
     a = np.clip(np.asarray(action, np.float64), -1.0, 1.0)
     tgt = q.copy()
+    tv = np.zeros_like(q)
     dofs = np.asarray(ctrl.dofs)
     lo, hi = model.lower[dofs], model.upper[dofs]
     if ctrl.mode == PD_JOINT_DELTA_POS:
         tgt[:, dofs] = np.clip(q[:, dofs] + a * ctrl.scale, lo, hi)
+        tv[:, dofs] = (tgt[:, dofs] - q[:, dofs]) * float(control_freq)
     elif ctrl.mode == PD_JOINT_POS:
         span_ok = np.isfinite(lo) & np.isfinite(hi)
         un = np.where(span_ok, lo + (a + 1.0) * 0.5 * (hi - lo), a * ctrl.scale)
@@ -236,26 +260,26 @@ def controller_targets(model, ctrl, q, action):
         LP, LQ = forward_kinematics(model, q)
         S = motion_subspace(model, LP, LQ)
         J = geometric_jacobian(model, S, ctrl.ee_link, LP[:, ctrl.ee_link])[:, :, dofs]
-        twist = np.concatenate([a[:, :3] * ctrl.scale, a[:, 3:6] * ctrl.rot_scale], -1)
+        w_ee = a[:, 3:6] * ctrl.rot_scale
+        twist = np.concatenate([a[:, :3] * ctrl.scale, se3.qrot(LQ[:, ctrl.ee_link], w_ee)], -1)
         dq = ik_delta(J, twist, ctrl.lam)
         tgt[:, dofs] = np.clip(q[:, dofs] + dq, lo, hi)
+        tv[:, dofs] = (tgt[:, dofs] - q[:, dofs]) * float(control_freq)
     elif ctrl.mode == "base_forward_rotate":
-        # controlled dofs 0,1,2 = base x, y, yaw; (forward, rotate) ->
-        # planar targets one control step ahead along the current heading
         a0, a1 = a[:, 0], a[:, 1]
         dx, dy, dyaw = dofs[0], dofs[1], dofs[2]
         yaw = q[:, dyaw]
-        step = a0 * ctrl.scale
-        tgt[:, dx] = np.clip(q[:, dx] + step * np.cos(yaw), model.lower[dx], model.upper[dx])
-        tgt[:, dy] = np.clip(q[:, dy] + step * np.sin(yaw), model.lower[dy], model.upper[dy])
-        tgt[:, dyaw] = np.clip(yaw + a1 * ctrl.rot_scale, model.lower[dyaw], model.upper[dyaw])
+        v = a0 * ctrl.scale
+        tv[:, dx] = v * np.cos(yaw)
+        tv[:, dy] = v * np.sin(yaw)
+        tv[:, dyaw] = a1 * ctrl.rot_scale
     else:
         raise NotImplementedError(ctrl.mode)
-    return tgt
+    return tgt, tv
 
 
 def control_step(model, st: State, drv: Drives, ctrl, action, cfg: SimConfig, want_contacts=False):
-    drv.target = controller_targets(model, ctrl, st.q, action)
+    drv.target, drv.target_vel = controller_targets(model, ctrl, st.q, action, cfg.control_freq)
     for _ in range(cfg.substeps):
         st = substep(model, st, drv, cfg, want_contacts)
     return st

@@ -260,12 +260,13 @@ class PickHeteroOracle:
     """PickHetero (BASELINE config 5): envs grouped by object layout, each group a
     PickCubeOracle over its global env ids (envs are independent)."""
 
-    def __init__(self, spec, descs, seed, cfg=None):
+    def __init__(self, spec, descs, seed, cfg=None, env_offset=0):
         self.B = len(descs)
         groups = {}
         for e, d in enumerate(descs):
             groups.setdefault(d.key(), (d, []))[1].append(e)
-        self.groups = [(np.asarray(idx), PickCubeOracle(spec, d, len(idx), seed, cfg=cfg, env_ids=idx))
+        self.groups = [(np.asarray(idx), PickCubeOracle(spec, d, len(idx), seed, cfg=cfg,
+                                                        env_ids=np.asarray(idx) + env_offset))
                        for d, idx in groups.values()]
 
     def step(self, action):

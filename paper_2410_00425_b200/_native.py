@@ -17,7 +17,7 @@ from .errors import raise_for_status
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_lib", "libbatchsim_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "batchsim_b200.h")
-ABI_VERSION = 7
+ABI_VERSION = 8
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
@@ -39,6 +39,16 @@ _SIGNATURES = {
     "bs_pose_transform_points_f32": [_P, _P, _I64, _P, _I64, _I64, _P, _P],
     "bs_pose_to_matrix_f64": [_P, _P, _I64, _P, _P],
     "bs_pose_from_matrix_f64": [_P, _I64, _P, _P, _P, _P],
+    "bs_quat_mul_f64": [_P, _I64, _P, _I64, _P, _P],
+    "bs_quat_mul_f32": [_P, _I64, _P, _I64, _P, _P],
+    "bs_quat_conjugate_f64": [_P, _I64, _P, _P],
+    "bs_quat_rotate_f64": [_P, _I64, _P, _I64, _P, _P],
+    "bs_quat_rotate_f32": [_P, _I64, _P, _I64, _P, _P],
+    "bs_quat_to_matrix_f64": [_P, _I64, _P, _P],
+    "bs_matrix_to_quat_f64": [_P, _I64, _P, _P],
+    "bs_tmat_compose_f64": [_P, _I64, _P, _I64, _P, _P],
+    "bs_tmat_inverse_f64": [_P, _I64, _P, _P],
+    "bs_tmat_transform_points_f64": [_P, _I64, _P, _I64, _I64, _P, _P],
 }
 
 _lib = None

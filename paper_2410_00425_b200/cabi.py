@@ -32,7 +32,7 @@ class BsStepOutputs(ctypes.Structure):
     _fields_ = [("obs", P), ("obs_dim", I32)] + [
         (n, P) for n in ("reward", "terminated", "truncated", "success", "fail", "unsupported_pairs",
                          "contact_count", "contact_pairs", "contact_geom", "ep_done", "ep_return_out",
-                         "ep_length_out", "ep_flags_out")]
+                         "ep_length_out", "ep_flags_out", "final_obs")]
 
 
 class BsSimParams(ctypes.Structure):
@@ -40,7 +40,8 @@ class BsSimParams(ctypes.Structure):
                 ("gravity", F64 * 3), ("friction", F64), ("beta", F64), ("slop", F64),
                 ("ctrl_mode", I32), ("action_dim", I32), ("action_scale", F64), ("action_scale_rot", F64), ("ik_lambda", F64),
                 ("ee_link", I32), ("task", I32), ("max_steps", I32), ("auto_reset", I32),
-                ("early_termination", I32), ("seed", ctypes.c_uint64), ("task_f", F64 * 16)]
+                ("early_termination", I32), ("seed", ctypes.c_uint64), ("task_f", F64 * 16),
+                ("control_freq", F64)]
 
 
 F32 = ctypes.c_float

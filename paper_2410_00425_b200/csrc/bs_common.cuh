@@ -3,6 +3,8 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <mutex>
 #include "../../include/batchsim_b200.h"
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
@@ -25,6 +27,42 @@ static inline int grid_for(int64_t n, int threads, int ctas_per_sm = 8) {
 static inline int launch_status() {
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? BS_OK : BS_ERR_CUDA;
+}
+
+// Per-device launcher state.  cudaFuncSetAttribute is per device, so the dynamic shared
+// memory opt-in a launcher has raised is remembered per (kernel slot, device); every access
+// is under one mutex so concurrent host threads (one per GPU) can launch safely.
+constexpr int kMaxDevices = 64;
+struct LaunchCache {
+  std::mutex mu;
+  size_t optin[8][kMaxDevices] = {};
+};
+static inline LaunchCache& launch_cache() {
+  static LaunchCache c;
+  return c;
+}
+static inline int current_device() {
+  int d = 0;
+  return cudaGetDevice(&d) == cudaSuccess && d >= 0 && d < kMaxDevices ? d : -1;
+}
+// Ensure `bytes` of dynamic shared memory are opted in on the current device for the kernel
+// group `slot` (set(bytes) applies the attribute to every kernel of the group).
+template <class Set>
+static inline bool ensure_smem_optin(int slot, size_t bytes, Set&& set) {
+  const int d = current_device();
+  if (d < 0) return false;
+  LaunchCache& c = launch_cache();
+  std::lock_guard<std::mutex> g(c.mu);
+  if (bytes <= c.optin[slot][d]) return true;
+  if (!set(bytes)) return false;
+  c.optin[slot][d] = bytes;
+  return true;
+}
+static inline int sm_count() {
+  const int d = current_device();
+  int n = 0;
+  if (d < 0 || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d) != cudaSuccess) return 0;
+  return n;
 }
 
 // Quaternion helpers in the reference's exact operation order

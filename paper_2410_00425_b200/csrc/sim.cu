@@ -58,7 +58,18 @@ __global__ void __launch_bounds__(64) k_reset(BsModelTables T, BsEnvState S, BsS
   EnvRegs<C> r;
   load_env<C>(T, S, M, e, r);
   Scratch<C> sc;
-  if (mask == nullptr || mask[e]) {
+  if (mask != nullptr && !mask[e]) {
+    // not selected: the env's state (its FK cache included) is left untouched bit for bit;
+    // only its state obs is re-emitted, from the cached link poses
+    if (O.obs) {
+      const R* lc = S.link_pose + (int64_t)e * T.L_max * 7;
+      for (int l = 0; l < M.L; ++l) { sc.lp[l] = ld3(lc + 7 * l); sc.lq[l] = ld4(lc + 7 * l + 3); }
+      pack_obs(M, P, T.D_max, T.A_max, r.q, r.qd, sc.lp, r.ap, r.aq, r.av, r.aw, r.goal,
+               O.obs + (int64_t)e * O.obs_dim, O.obs_dim);
+    }
+    return;
+  }
+  {
     uint32_t rc = S.reset_count[e] + (bump ? 1u : 0u);
     S.reset_count[e] = rc;
     int32_t tdof = -1;
@@ -69,9 +80,6 @@ __global__ void __launch_bounds__(64) k_reset(BsModelTables T, BsEnvState S, BsS
     if (S.ep_return) S.ep_return[e] = 0.0;
     if (S.ep_flags) S.ep_flags[e] = 0;
     for (int i = 0; i < M.D; ++i) r.tgt[i] = r.q[i];
-  } else {
-    const R* tg = S.target + (int64_t)e * T.D_max;
-    for (int i = 0; i < M.D; ++i) r.tgt[i] = tg[i];
   }
   fk<C>(M, r.q, sc.lp, sc.lq);
   store_env<C>(T, S, M, e, r, sc.lp, sc.lq);

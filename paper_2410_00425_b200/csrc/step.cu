@@ -73,7 +73,7 @@ __device__ long long g_bs_last;
 // maxima; identical for every env of the launch).
 struct Lay {
   int Dm, Lm, Sm, Cm, Am, NU, RW, KCH;
-  int q, qd, tgt, apose, avel, goal;
+  int q, qd, tgt, tgtv, apose, avel, goal;
   int lpq, Sv, In, Mt, Minv, cb, u, Iwi, spq;
   int Tl, V, Ac, F, ct, rows;
   int total;
@@ -93,10 +93,11 @@ struct Lay {
 
 // EX_ = the launch guarantees D_max == MD and A_max == MA exactly, so the padded widths
 // (D_max, A_max, NU and the row stride) are compile-time constants in the kernel.
-template <int G_, int MD_, int MA_, bool EX_ = false>
+template <int G_, int MD_, int MA_, bool EX_ = false, int SLOT_ = 1>
 struct Cfg {
   static constexpr int G = G_, MD = MD_, MA = MA_, EPW = 32 / G_, NU = MD_ + 6 * MA_;
   static constexpr bool EXACT = EX_;
+  static constexpr int SLOT = SLOT_;  // bs::LaunchCache slot of this variant's smem opt-in
 };
 
 __device__ __forceinline__ R sgn_of(R v) { return v > 0.0 ? 1.0 : -1.0; }
@@ -369,6 +370,10 @@ __device__ __noinline__ void ee_delta_targets(const Model M, const BsSimParams& 
     const R aj = fmin(fmax((R)act[j], -1.0), 1.0);
     tw[j] = aj * (j < 3 ? P.action_scale : P.action_scale_rot);
   }
+  {  // the rotation action is an axis-angle in the EE frame: rotate it to the world
+    const V3<R> w = quat_rotate(ld4(lpq0 + 7 * P.ee_link + 3), v3(tw[3], tw[4], tw[5]));
+    tw[3] = w.x; tw[4] = w.y; tw[5] = w.z;
+  }
   const R lam2 = P.ik_lambda * P.ik_lambda;
   for (int i = 0; i < 6; ++i)
     for (int j = 0; j <= i; ++j) {
@@ -407,6 +412,7 @@ __device__ __noinline__ void ee_delta_targets(const Model M, const BsSimParams& 
       tgt = fmin(fmax(qi + dq, M.lower[d]), M.upper[d]);
     }
     E[Y.tgt + d] = tgt;
+    E[Y.tgtv + d] = (tgt - qi) * P.control_freq;  // the delta is a motion over one control period
   }
     }
 
@@ -549,13 +555,16 @@ __device__ __forceinline__ void substep(const Model& M, const BsSimParams& P, co
   }
   __syncwarp();
   BS_TICK(7);
-  // ---- F: implicit PD drives (A-16) and Cholesky of Mt (lane 0; inverse diagonal kept)
+  // ---- F: implicit PD drives (A-16) and Cholesky of Mt (lane 0; inverse diagonal kept).
+  // tau = Kp (q* - q) + Kd (qd* - qd) with the gains per unit inertia scale
+  // (SPEC.md:427): Kp = kp M_ii, Kd = kd M_ii, evaluated at the end-of-substep velocity.
   if (l == 0) {
     for (int i = 0; i < D; ++i) {
-      const R kp = M.kp[i], kd = M.kd[i], dmp = M.damping[i], fl = M.flim[i];
+      const R mii = Mt[i * Dm + i];
+      const R kp = M.kp[i] * mii, kd = M.kd[i] * mii, dmp = M.damping[i], fl = M.flim[i];
       const R qi = E[Y.q + i], qdi = E[Y.qd + i];
-      Mt[i * Dm + i] += dt * (kd + dmp) + (dt * dt) * kp;
-      R tau = kp * ((E[Y.tgt + i] - qi) - dt * qdi) + kd * (0.0 - qdi);
+      Mt[i * Dm + i] = mii + (dt * (kd + dmp) + (dt * dt) * kp);
+      R tau = kp * ((E[Y.tgt + i] - qi) - dt * qdi) + kd * (E[Y.tgtv + i] - qdi);
       tau = fmin(fmax(tau, -fl), fl) - dmp * qdi;
       cb[i] = tau - cb[i];
     }
@@ -939,6 +948,30 @@ __device__ __forceinline__ void substep(const Model& M, const BsSimParams& P, co
   BS_TICK(14);
 }
 
+// The state observation of the env staged in E (group lanes cooperate).  Layout (DESIGN.md
+// "State observation"): q[D_max] qd[D_max] ee_p[3], per actor slot p[3] q[4] v[3] w[3],
+// goal[3], zero padding; CartpoleBalance: (x, x_dot, theta, theta_dot).
+template <int G>
+__device__ __forceinline__ void pack_state_obs(const Model& M, const BsSimParams& P, const Lay& Y, const R* E,
+                                               float* o, int obs_dim, int Dm, int Ag, int l) {
+  const R* lpq = E + Y.lpq;
+  const int b_ee = 2 * Dm, b_act = b_ee + 3, b_goal = b_act + 13 * Ag;
+  const bool cart = P.task == BS_TASK_CARTPOLE;
+  #pragma unroll 1
+  for (int k = l; k < obs_dim; k += G) {
+    R v = 0.0;
+    if (cart) v = k < 4 ? E[(k & 1 ? Y.qd : Y.q) + (k >> 1)] : 0.0;
+    else if (k < Dm) v = k < M.D ? E[Y.q + k] : 0.0;
+    else if (k < b_ee) v = (k - Dm) < M.D ? E[Y.qd + k - Dm] : 0.0;
+    else if (k < b_act) v = P.ee_link >= 0 ? lpq[7 * P.ee_link + (k - b_ee)] : 0.0;
+    else if (k < b_goal) {
+      const int a = (k - b_act) / 13, j = (k - b_act) - 13 * a;
+      if (a < M.A) v = j < 7 ? E[Y.apose + 7 * a + j] : E[Y.avel + 6 * a + (j - 7)];
+    } else if (k < b_goal + 3) v = E[Y.goal + (k - b_goal)];
+    o[k] = (float)v;
+  }
+}
+
 // ------------------------------------------------------------------ the kernel
 template <class K>
 __global__ void __launch_bounds__(32) k_step(const __grid_constant__ BsModelTables T, const __grid_constant__ BsEnvState S,
@@ -979,9 +1012,10 @@ __global__ void __launch_bounds__(32) k_step(const __grid_constant__ BsModelTabl
     fk_group<G>(M, Y, E, l);
     if (l == 0) ee_delta_targets(M, P, Y, E, act);
   } else if (P.ctrl_mode == BS_CTRL_BASE_FORWARD_ROTATE) {
-    // mobile base: controlled dofs 0, 1, 2 = base x, y, yaw; the action
-    // (forward, rotate) in [-1, 1] becomes planar targets one control step ahead along the
-    // current heading: x* = x + a0 s cos(yaw), y* = y + a0 s sin(yaw), yaw* = yaw + a1 s_rot
+    // mobile base: controlled dofs 0, 1, 2 = base x, y, yaw, driven
+    // kinematically through VELOCITY targets: the action (forward, rotate) in [-1, 1] becomes
+    // (a0 s cos(yaw), a0 s sin(yaw), a1 s_rot) m/s, m/s, rad/s; the position targets stay at q
+    // (the base dofs carry kp = 0, a pure velocity servo)
     __syncwarp();  // E[q] is staged by the other lanes
     if (l == 0) {
       int bd[3] = {-1, -1, -1};
@@ -993,29 +1027,31 @@ __global__ void __launch_bounds__(32) k_step(const __grid_constant__ BsModelTabl
       const R yaw = bd[2] >= 0 ? E[Y.q + bd[2]] : 0.0;
       R sy, cy;
       sincos(yaw, &sy, &cy);
-      for (int d = 0; d < M.D; ++d) E[Y.tgt + d] = E[Y.q + d];
-      const R stp = a0 * P.action_scale;
-      if (bd[0] >= 0) E[Y.tgt + bd[0]] = fmin(fmax(E[Y.q + bd[0]] + stp * cy, M.lower[bd[0]]), M.upper[bd[0]]);
-      if (bd[1] >= 0) E[Y.tgt + bd[1]] = fmin(fmax(E[Y.q + bd[1]] + stp * sy, M.lower[bd[1]]), M.upper[bd[1]]);
-      if (bd[2] >= 0) E[Y.tgt + bd[2]] = fmin(fmax(yaw + a1 * P.action_scale_rot, M.lower[bd[2]]), M.upper[bd[2]]);
+      for (int d = 0; d < M.D; ++d) { E[Y.tgt + d] = E[Y.q + d]; E[Y.tgtv + d] = 0.0; }
+      const R v = a0 * P.action_scale;
+      if (bd[0] >= 0) E[Y.tgtv + bd[0]] = v * cy;
+      if (bd[1] >= 0) E[Y.tgtv + bd[1]] = v * sy;
+      if (bd[2] >= 0) E[Y.tgtv + bd[2]] = a1 * P.action_scale_rot;
     }
   } else {
     #pragma unroll 1
     for (int i = l; i < M.D; i += G) {
       const int ai = M.ctrl[i];
       const R qi = S.qpos[(int64_t)e * Dm + i];
-      R tgt = qi;
+      R tgt = qi, tgtv = 0.0;
       if (ai >= 0) {
         const R a = fmin(fmax((R)act[ai], -1.0), 1.0);
         const R lo = M.lower[i], hi = M.upper[i];
         if (P.ctrl_mode == BS_CTRL_PD_JOINT_DELTA_POS) {
           tgt = fmin(fmax(qi + a * P.action_scale, lo), hi);
+          tgtv = (tgt - qi) * P.control_freq;  // the delta is a motion over one control period
         } else {
           const R un = (isfinite(lo) && isfinite(hi)) ? lo + (a + 1.0) * 0.5 * (hi - lo) : a * P.action_scale;
           tgt = fmin(fmax(un, lo), hi);
         }
       }
       E[Y.tgt + i] = tgt;
+      E[Y.tgtv + i] = tgtv;
     }
   }
   bool diverged = S.diverged[e] != 0;
@@ -1101,6 +1137,9 @@ __global__ void __launch_bounds__(32) k_step(const __grid_constant__ BsModelTabl
   }
   // ---- in-kernel auto-reset from the env's Philox stream
   const bool done = live && P.auto_reset && (terminated || truncated);
+  // the observation of the state the episode ENDED in, before the reset replaces it (lets a
+  // learner bootstrap V(s_T) on time-limit truncations)
+  if (done && O.final_obs) pack_state_obs<G>(M, P, Y, E, O.final_obs + (int64_t)e * O.obs_dim, O.obs_dim, Dm, Ag, l);
   uint8_t div_out = diverged;
   if (__any_sync(FULLMASK, done)) {
     if (done && l == 0) {
@@ -1143,26 +1182,7 @@ __global__ void __launch_bounds__(32) k_step(const __grid_constant__ BsModelTabl
     S.elapsed[e] = el;
     S.diverged[e] = div_out;
   }
-  if (O.obs) {
-    // layout: q[D_max] qd[D_max] ee_p[3]
-    //   per actor slot: p[3] q[4] v[3] w[3]   goal[3]   zero padding
-    float* o = O.obs + (int64_t)e * O.obs_dim;
-    const int b_ee = 2 * Dm, b_act = b_ee + 3, b_goal = b_act + 13 * Ag;
-    const bool cart = P.task == BS_TASK_CARTPOLE;
-    #pragma unroll 1
-    for (int k = l; k < O.obs_dim; k += G) {
-      R v = 0.0;
-      if (cart) v = k < 4 ? E[(k & 1 ? Y.qd : Y.q) + (k >> 1)] : 0.0;
-      else if (k < Dm) v = k < M.D ? E[Y.q + k] : 0.0;
-      else if (k < b_ee) v = (k - Dm) < M.D ? E[Y.qd + k - Dm] : 0.0;
-      else if (k < b_act) v = P.ee_link >= 0 ? lpq[7 * P.ee_link + (k - b_ee)] : 0.0;
-      else if (k < b_goal) {
-        const int a = (k - b_act) / 13, j = (k - b_act) - 13 * a;
-        if (a < M.A) v = j < 7 ? E[Y.apose + 7 * a + j] : E[Y.avel + 6 * a + (j - 7)];
-      } else if (k < b_goal + 3) v = E[Y.goal + (k - b_goal)];
-      o[k] = (float)v;
-    }
-  }
+  if (O.obs) pack_state_obs<G>(M, P, Y, E, O.obs + (int64_t)e * O.obs_dim, O.obs_dim, Dm, Ag, l);
   BS_TICK(17);
   BS_CTA_END;
 }
@@ -1179,6 +1199,7 @@ static Lay make_lay(const BsModelTables& T, int G) {
   y.q = o; o += y.Dm;
   y.qd = o; o += y.Dm;
   y.tgt = o; o += y.Dm;
+  y.tgtv = o; o += y.Dm;
   y.apose = o; o += 7 * y.Am;
   y.avel = o; o += 6 * y.Am;
   y.goal = o; o += 3;
@@ -1213,20 +1234,25 @@ template <class K>
 static int launch(const BsModelTables& T, const BsEnvState& S, const BsStepOutputs& O, const BsSimParams& P,
                   const float* action, cudaStream_t st) {
   Lay y = make_lay(T, K::G);
-  static size_t attr_bytes = 0;  // opt-in above 48 KB, raised on demand
+  // opt-in above 48 KB, raised on demand per device (kernel group slot 1 + variant)
   auto ensure_attr = [](size_t b) {
-    if (b <= attr_bytes) return true;
-    if (cudaFuncSetAttribute(k_step<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b) != cudaSuccess)
-      return false;
-    attr_bytes = b;
-    return true;
+    return bs::ensure_smem_optin(K::SLOT, b, [](size_t v) {
+      return cudaFuncSetAttribute(k_step<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v) == cudaSuccess;
+    });
   };
   // Pad the per-env stride to 2 (mod 16) doubles when that costs no residency: the groups of a
-  // warp then sit in distinct 16-byte bank slots for the sweep's broadcast loads.
-  static int last_key[5] = {-1, -1, -1, -1, -1}, last_total = 0;
+  // warp then sit in distinct 16-byte bank slots for the sweep's broadcast loads.  The choice
+  // is a pure function of (layout widths, kernel variant), cached per variant.
+  struct StrideMemo { std::mutex mu; int key[5] = {-1, -1, -1, -1, -1}; int total = 0; };
+  static StrideMemo memo;
   const int key[5] = {y.Dm, y.Lm, y.Sm, y.Cm, y.Am};
-  if (memcmp(key, last_key, sizeof(key)) == 0) {
-    y.total = last_total;
+  int cached = -1;
+  {
+    std::lock_guard<std::mutex> g(memo.mu);
+    if (memcmp(key, memo.key, sizeof(key)) == 0) cached = memo.total;
+  }
+  if (cached >= 0) {
+    y.total = cached;
   } else {
     const int padded = y.total + ((2 - y.total % 16) + 16) % 16;
     const size_t b0 = (size_t)K::EPW * y.total * sizeof(double), b1 = (size_t)K::EPW * padded * sizeof(double);
@@ -1236,8 +1262,9 @@ static int launch(const BsModelTables& T, const BsEnvState& S, const BsStepOutpu
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n1, k_step<K>, 32, b1);
       if (n1 >= n0) y.total = padded;
     }
-    memcpy(last_key, key, sizeof(key));
-    last_total = y.total;
+    std::lock_guard<std::mutex> g(memo.mu);
+    memcpy(memo.key, key, sizeof(key));
+    memo.total = y.total;
   }
   const size_t bytes = (size_t)K::EPW * y.total * sizeof(double);
   if (bytes > 220 * 1024) return BS_ERR_UNSUPPORTED;
@@ -1247,10 +1274,10 @@ static int launch(const BsModelTables& T, const BsEnvState& S, const BsStepOutpu
   return launch_status();
 }
 
-typedef Cfg<8, 3, 1, true> CfgPick;  // exactly ARM3 + one free actor (PickCube, PickHetero): static widths
-typedef Cfg<8, 4, 1> CfgSmall;    // PickCube-style: D <= 4, one free actor
-typedef Cfg<8, 12, 1> CfgArt;     // articulated objects (arm + cabinet): D <= 12, <= 1 actor
-typedef Cfg<8, 12, 4> CfgLarge;   // general scenes: D <= 12, <= 4 actors
+typedef Cfg<8, 3, 1, true, 1> CfgPick;  // exactly ARM3 + one free actor (PickCube, PickHetero): static widths
+typedef Cfg<8, 4, 1, false, 2> CfgSmall;    // PickCube-style: D <= 4, one free actor
+typedef Cfg<8, 12, 1, false, 3> CfgArt;     // articulated objects (arm + cabinet): D <= 12, <= 1 actor
+typedef Cfg<8, 12, 4, false, 4> CfgLarge;   // general scenes: D <= 12, <= 4 actors
 
 }  // namespace step
 }  // namespace bs

@@ -184,7 +184,7 @@ class CartpoleSpec:
     fail_x: float = 1.7
     max_steps: int = 200
     control_mode: str = "pd_joint_delta_pos"
-    action_scale: float = 0.05
+    action_scale: float = 0.01   # m per unit action (target velocity = 0.6 m/s per unit action)
     kp: float = 1000.0
     kd: float = 2.0 * math.sqrt(1000.0)
     force_limit: float = 100.0

@@ -28,23 +28,45 @@ STAT_FIELDS = ("episodes", "return_sum", "length_sum", "success_once", "success_
                "fail_at_end")
 
 
+def _all_reduce(t: torch.Tensor, op, group=None) -> torch.Tensor:
+    """In-place all-reduce; through host memory when the backend cannot reduce device tensors
+    (gloo: the multi-rank smoke runs on one GPU and the CPU tests)."""
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1):
+        return t
+    if t.is_cuda and dist.get_backend(group) != "nccl":
+        h = t.cpu()
+        dist.all_reduce(h, op=op, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=op, group=group)
+    return t
+
+
 def reduce_stats(stats: torch.Tensor, group=None) -> torch.Tensor:
-    """SUM all-reduce of a (len(STAT_FIELDS),) float64 statistics vector across ranks; a no-op
+    """SUM all-reduce of a statistics vector (e.g. STAT_FIELDS, float64) across ranks; a no-op
     when torch.distributed is not initialised."""
     import torch.distributed as dist
 
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(stats, op=dist.ReduceOp.SUM, group=group)
-    return stats
+    return _all_reduce(stats, dist.ReduceOp.SUM, group)
 
 
 def max_over_ranks(values: torch.Tensor, group=None) -> torch.Tensor:
     """Element-wise MAX across ranks (timings: the job is as slow as its slowest rank)."""
     import torch.distributed as dist
 
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(values, op=dist.ReduceOp.MAX, group=group)
-    return values
+    return _all_reduce(values, dist.ReduceOp.MAX, group)
+
+
+def describe(group=None) -> dict:
+    """Communicator facts for logs: backend, world size, rank (None when not initialised)."""
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()):
+        return {"backend": None, "world_size": 1, "rank": 0}
+    return {"backend": dist.get_backend(group), "world_size": dist.get_world_size(group),
+            "rank": dist.get_rank(group)}
 
 
 def summarize(stats: torch.Tensor) -> dict:

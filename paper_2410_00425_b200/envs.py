@@ -74,6 +74,7 @@ class Env:
         p = cabi.BsSimParams()
         p.dt = 1.0 / self.sim.sim_freq
         p.substeps = self.sim.sim_freq // self.sim.control_freq
+        p.control_freq = float(self.sim.control_freq)
         p.pos_iters, p.vel_iters = self.sim.solver_pos_iters, self.sim.solver_vel_iters
         for i in range(3):
             p.gravity[i] = self.sim.gravity[i]
@@ -110,6 +111,8 @@ class Env:
         self.ep_return_out = torch.zeros(N, dtype=torch.float64, device=dev)
         self.ep_length_out = torch.zeros(N, dtype=torch.int32, device=dev)
         self.ep_flags_out = torch.zeros(N, dtype=torch.uint8, device=dev)
+        # state obs of the state an episode ended in (written for auto-reset envs only)
+        self.final_obs = torch.zeros((N, self.obs_dim), dtype=torch.float32, device=dev)
         o = cabi.BsStepOutputs()
         o.obs, o.obs_dim = self.state_obs.data_ptr(), self.obs_dim
         for k, t in (("reward", self.reward), ("terminated", self.terminated), ("truncated", self.truncated),
@@ -117,11 +120,13 @@ class Env:
                      ("contact_count", self.contact_count), ("contact_pairs", self.contact_pairs),
                      ("contact_geom", self.contact_geom), ("ep_done", self.ep_done),
                      ("ep_return_out", self.ep_return_out), ("ep_length_out", self.ep_length_out),
-                     ("ep_flags_out", self.ep_flags_out)):
+                     ("ep_flags_out", self.ep_flags_out), ("final_obs", self.final_obs)):
             setattr(o, k, t.data_ptr())
         self.c_out = o
         self._graph = None
-        self._graph_stream = None
+        self._graph_key = None
+        self._host_graph = None
+        self._host_graph_key = None
 
     # ------------------------------------------------------------------ spaces
     @property
@@ -188,7 +193,7 @@ class Env:
         else:
             ptr = a.data_ptr()
         if self._graph is not None:
-            self._graph.replay()
+            self._replay()
         else:
             self._launch_step(ptr)
         return self._result()
@@ -203,7 +208,7 @@ class Env:
     def launch_step(self) -> None:
         """Enqueue one step on the static action buffer (no validation, no host work)."""
         if self._graph is not None:
-            self._graph.replay()
+            self._replay()
         else:
             self._launch_step(self.action_buf.data_ptr())
 
@@ -213,63 +218,96 @@ class Env:
         self.launch_step()
         return self._result()
 
-    def capture_graph(self, warmup: int = 2) -> None:
-        """Capture bs_step (+ render) on the static action buffer into a CUDA graph."""
-        s = torch.cuda.Stream(device=self.device)
-        s.wait_stream(torch.cuda.current_stream(self.device))
-        snap = self.scene.get_state()
-        with torch.cuda.stream(s):
-            for _ in range(warmup):
-                self._launch_step(self.action_buf.data_ptr())
-        torch.cuda.current_stream(self.device).wait_stream(s)
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            self._launch_step(self.action_buf.data_ptr())
+    # ------------------------------------------------------------------ CUDA graphs
+    # A graph bakes in the BsSimParams it was captured with (bs_step takes them by value into
+    # the kernel's constant bank).  Every graph records the params bytes it was captured
+    # with; a step whose params differ (reset(seed=...), eval_wrapper, a user edit) re-captures
+    # before replaying, so a graph never replays stale seeds or reset/termination modes.
+
+    def _params_key(self) -> bytes:
+        return bytes(self.c_params)
+
+    def _side_effect_buffers(self):
+        """Every device buffer a step writes outside the scene state rows."""
+        bufs = [self._out_arena, self.unsupported, self.contact_count, self.contact_pairs, self.contact_geom,
+                self.ep_done, self.ep_return_out, self.ep_length_out, self.ep_flags_out, self.final_obs]
+        if self.renderer is not None:
+            for g in self.renderer.groups:
+                bufs += [g[k] for k in ("rgb", "depth", "seg", "pc") if g[k] is not None]
+        return bufs
+
+    def _warm_launchers(self, launch) -> None:
+        """Run `launch` once eagerly so every launcher has configured its kernels (shared-memory
+        opt-in, occupancy queries) before a capture, then restore EVERYTHING it wrote: the
+        scene state and every output buffer -- the warmup leaves no trace."""
+        if getattr(self, "_warmed", False):
+            return
+        cur = torch.cuda.current_stream(self.device)
+        snap = self.scene.get_state()                      # queued on the current stream first
+        saved = [b.clone() for b in self._side_effect_buffers()]
+        launch()                                           # same stream: ordered after the snapshot
         self.scene.set_state(snap)
-        self._graph = g
+        for b, v in zip(self._side_effect_buffers(), saved):
+            b.copy_(v)
+        cur.synchronize()
+        self._warmed = True
+
+    def _capture(self, launch) -> "torch.cuda.CUDAGraph":
+        self._warm_launchers(launch)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):   # capture records, it does not execute: no state changes
+            launch()
+        return g
+
+    def capture_graph(self, warmup: int = 1) -> None:
+        """Capture bs_step (+ render) on the static action buffer into a CUDA graph."""
+        self._graph = self._capture(lambda: self._launch_step(self.action_buf.data_ptr()))
+        self._graph_key = self._params_key()
+
+    def _replay(self) -> None:
+        if self._graph_key != self._params_key():
+            self.capture_graph()
+        self._graph.replay()
 
     # ------------------------------------------------------------------ host I/O path
-    def enable_host_io(self, warmup: int = 2) -> None:
+    def enable_host_io(self, warmup: int = 1) -> None:
         """Capture [step reading the host actions and writing obs/reward/flags to host memory
         (zero-copy over PCIe), render, D2H of the frames] as ONE CUDA graph over pinned host
         buffers, for callers that keep actions and observations on the host (``step_host``).
         The device-side API (``step``) is unaffected; in host-I/O steps the device copies of
         obs/reward/flags are not written."""
         N, A = self.num_envs, max(1, self.action_dim)
-        self._h_action = torch.zeros((N, A), dtype=torch.float32).pin_memory()
-        outs = self._host_outputs()
-        # the arena's tensors come back in one copy; frames (render modes) one copy each
-        self._h_arena = torch.zeros(self._out_arena.numel(), dtype=torch.uint8).pin_memory()
-        hv = self._arena_views(self._h_arena)
-        in_arena = {k: ("obs" if k in ("obs", "obs/state") else k) for k in outs
-                    if k in ("obs", "obs/state", "reward", "terminated", "truncated", "success", "fail")}
-        self._h_outs = {k: hv[in_arena[k]] if k in in_arena else torch.empty(v.shape, dtype=v.dtype).pin_memory()
-                        for k, v in outs.items()}
-        s = torch.cuda.Stream(device=self.device)
-        s.wait_stream(torch.cuda.current_stream(self.device))
-        snap = self.scene.get_state()
-        with torch.cuda.stream(s):
-            for _ in range(warmup):
-                self._launch_step(self.action_buf.data_ptr())
-        torch.cuda.current_stream(self.device).wait_stream(s)
-        # zero-copy: the step kernel reads the actions from, and writes obs / reward / flags to,
-        # the pinned host buffers directly over PCIe (page-locked memory is device-addressable
-        # under UVA), so the graph has no H2D/D2H copy nodes for them; frames are still copied
-        self._c_out_host = cabi.BsStepOutputs.from_buffer_copy(self.c_out)
-        for k in ("reward", "terminated", "truncated", "success", "fail"):
-            setattr(self._c_out_host, k, hv[k].data_ptr())
-        self._c_out_host.obs = hv["obs"].data_ptr()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
+        if getattr(self, "_h_action", None) is None:
+            self._h_action = torch.zeros((N, A), dtype=torch.float32).pin_memory()
+            outs = self._host_outputs()
+            # the arena's tensors come back in one copy; frames (render modes) one copy each
+            self._h_arena = torch.zeros(self._out_arena.numel(), dtype=torch.uint8).pin_memory()
+            hv = self._arena_views(self._h_arena)
+            self._h_in_arena = {k: ("obs" if k in ("obs", "obs/state") else k) for k in outs
+                                if k in ("obs", "obs/state", "reward", "terminated", "truncated", "success", "fail")}
+            self._h_outs = {k: hv[self._h_in_arena[k]] if k in self._h_in_arena
+                            else torch.empty(v.shape, dtype=v.dtype).pin_memory() for k, v in outs.items()}
+            self._h_dev_outs = outs
+            # zero-copy: the step kernel reads the actions from, and writes obs / reward / flags to,
+            # the pinned host buffers directly over PCIe (page-locked memory is device-addressable
+            # under UVA), so the graph has no H2D/D2H copy nodes for them; frames are still copied
+            self._c_out_host = cabi.BsStepOutputs.from_buffer_copy(self.c_out)
+            for k in ("reward", "terminated", "truncated", "success", "fail"):
+                setattr(self._c_out_host, k, hv[k].data_ptr())
+            self._c_out_host.obs = hv["obs"].data_ptr()
+
+        def launch():
             nat.call("bs_step", ctypes.byref(self.scene.c_tables), ctypes.byref(self.scene.c_state),
                      ctypes.byref(self._c_out_host), ctypes.byref(self.c_params), self._h_action.data_ptr(),
                      nat.stream_handle())
             self._render()
-            for k, v in outs.items():
-                if k not in in_arena:
+            for k, v in self._h_dev_outs.items():
+                if k not in self._h_in_arena:
                     self._h_outs[k].copy_(v, non_blocking=True)
-        self.scene.set_state(snap)
-        self._host_graph = g
+
+        self._warm_launchers(lambda: self._launch_step(self.action_buf.data_ptr()))
+        self._host_graph = self._capture(launch)
+        self._host_graph_key = self._params_key()
 
     def _arena_bytes(self) -> int:
         n = 0
@@ -316,6 +354,8 @@ class Env:
         if self.validate_actions and not np.isfinite(a).all():
             raise InputError("non-finite action")
         self._h_action.numpy()[:, :self.action_dim] = a
+        if self._host_graph_key != self._params_key():
+            self.enable_host_io()
         self._host_graph.replay()
         torch.cuda.current_stream(self.device).synchronize()
         return self._h_outs
@@ -338,6 +378,8 @@ class Env:
         info = {"success": self.success, "fail": self.fail, "unsupported_pairs": self.unsupported,
                 "elapsed": self.scene.elapsed, "diverged": self.scene.diverged,
                 "contact_count": self.contact_count,
+                # rows of envs auto-reset this step: the state obs the episode ended in
+                "final_obs": self.final_obs,
                 "episode": {"done": self.ep_done, "return": self.ep_return_out, "length": self.ep_length_out,
                             "flags": self.ep_flags_out}}
         return StepResult(self._obs(), self.reward, self.terminated, self.truncated, info)

@@ -110,6 +110,44 @@ def _arm3() -> str:
 ARM3_URDF = _arm3()
 
 
+def make_arm6_urdf(name: str = "arm6") -> str:
+    """6-DOF arm for the full-twist pd_ee_delta_pose KAT ("a reachable arm"): ARM3's
+    yaw / shoulder / elbow and links, then a spherical wrist at the forearm tip (roll about x,
+    pitch about y, roll about x; concentric axes) and the ee sphere 0.1 m beyond it.  A 3-DOF
+    arm cannot follow a 6-D twist (DLS trades the rotation rows); this one can."""
+    seg = lambda n, m, iyy: _link(  # noqa: E731
+        n, _inertial(m, ("0.001", iyy, iyy), "0.2 0 0"),
+        _collision(_capsule("0.03", "0.32"), xyz="0.2 0 0", rpy=f"0 {HALF_PI} 0"))
+    small = lambda n: _link(n, _inertial("0.1", ("0.0002", "0.0002", "0.0002")))  # noqa: E731
+    return _robot(name, [
+        _link("root"),
+        _link("shoulder_link", _inertial("0.5", ("0.002", "0.002", "0.002"))),
+        seg("upper_arm", "0.8", "0.012"),
+        seg("forearm", "0.6", "0.009"),
+        small("wrist_roll_link"),
+        small("wrist_pitch_link"),
+        _link("hand", _inertial("0.1", ("0.0002", "0.0002", "0.0002"), "0.05 0 0")),
+        _link("ee", _inertial("0.05", ("0.0001", "0.0001", "0.0001")),
+              _collision('<sphere radius="0.03"/>'), color="0.9 0.2 0.2 1"),
+    ], [
+        _joint("yaw", "revolute", "root", "shoulder_link", axis="0 0 1", limit=("-3.1", "3.1"), damping="0.1"),
+        _joint("shoulder", "revolute", "shoulder_link", "upper_arm", axis="0 1 0", limit=("-2.2", "2.2"),
+               damping="0.1"),
+        _joint("elbow", "revolute", "upper_arm", "forearm", axis="0 1 0", xyz="0.4 0 0",
+               limit=("-2.4", "2.4"), damping="0.1"),
+        _joint("wrist_roll", "revolute", "forearm", "wrist_roll_link", axis="1 0 0", xyz="0.4 0 0",
+               limit=("-3.1", "3.1"), damping="0.05"),
+        _joint("wrist_pitch", "revolute", "wrist_roll_link", "wrist_pitch_link", axis="0 1 0",
+               limit=("-2.0", "2.0"), damping="0.05"),
+        _joint("wrist_roll2", "revolute", "wrist_pitch_link", "hand", axis="1 0 0", limit=("-3.1", "3.1"),
+               damping="0.05"),
+        _joint("ee_weld", "fixed", "hand", "ee", xyz="0.1 0 0"),
+    ])
+
+
+ARM6_URDF = make_arm6_urdf()
+
+
 def _gantry(name, carriages, tip, axes, limits, tip_shape=None, tip_color=None):
     links = [_link("frame")]
     for cname, mass, inert in carriages:

@@ -328,6 +328,11 @@ def ppo_train(env, cfg: PPOConfig, seed: int = 0, eval_env=None, time_limit: Opt
             r = env.step(a.clamp(-1.0, 1.0).contiguous())
             buf_rew[t] = r.reward
             buf_done[t] = (r.terminated | r.truncated).to(dtype)
+            # a time-limit truncation is not a terminal state: bootstrap gamma * V(s_T) from the
+            # observation the episode ended in (the kernel exports it before the auto-reset)
+            trunc = (r.truncated.bool() & ~r.terminated.bool()).to(dtype)
+            _, _, v_fin, _ = net.forward(rms.normalize(r.info["final_obs"].to(dtype), cfg.obs_clip))
+            buf_rew[t] += cfg.gamma * v_fin * trunc
             obs = r.obs
         _, _, last_v, _ = net.forward(rms.normalize(obs.to(dtype), cfg.obs_clip))
         adv, ret = compute_gae(buf_rew, buf_val, buf_done, last_v, cfg.gamma, cfg.gae_lambda)

@@ -90,10 +90,10 @@ class MetricsSink:
 def eval_wrapper(env):
     """Evaluation mode: terminated is never raised early and envs are not
     auto-reset, so every episode runs to its time limit; metrics are emitted at truncation.
-    Mutates and returns `env` (a captured CUDA graph is dropped: the params are baked in)."""
+    Mutates and returns `env`; captured CUDA graphs (device and host-I/O) are re-captured on
+    their next replay because the params they baked in changed (envs.Env._replay)."""
     env.c_params.early_termination = 0
     env.c_params.auto_reset = 0
-    env._graph = None
     env.eval_mode = True
     return env
 

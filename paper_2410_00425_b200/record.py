@@ -16,7 +16,9 @@ the identical state trajectory) without altering dynamics.
 
 from __future__ import annotations
 
+import dataclasses
 import json
+import math
 import os
 import time
 
@@ -57,8 +59,16 @@ def record(env, policy, steps: int, path: str, source: str = "policy", store_sta
         if store_states:
             for k in STATE_STREAM:
                 states[k].append(getattr(env.scene, k).clone())
+    cams = getattr(env, "custom_cameras", None)
     manifest = {"engine": __version__, "abi": nat.ABI_VERSION, "task": getattr(env, "task_name", env.name),
                 "overrides": getattr(env, "overrides", {}), "num_envs": env.num_envs, "seed": env.seed,
+                # everything else make_task and the env were given: the global batch and this shard,
+                # the SimConfig, custom cameras and the full step params (eval mode, reset policy ...)
+                "global_num_envs": getattr(env, "global_num_envs", env.num_envs),
+                "shard": list(env.shard) if getattr(env, "shard", None) else None,
+                "env_offset": env.scene.env_offset, "sim": dataclasses.asdict(env.sim),
+                "cameras": [dataclasses.asdict(c) for c in cams] if cams else None,
+                "c_params": _struct_dict(env.c_params),
                 "obs_mode": env.obs_mode, "layout_hash": env.scene.layout_hash,
                 "controller": {"mode": env.scene.control.mode, "action_scale": env.scene.control.action_scale},
                 "action_dim": env.action_dim, "steps": steps, "source": source, "created": time.time(),
@@ -76,6 +86,38 @@ def record(env, policy, steps: int, path: str, source: str = "policy", store_sta
     with open(os.path.join(path, "manifest.json"), "w") as f:
         json.dump(manifest, f, indent=1, sort_keys=True)
     return manifest
+
+
+def _struct_dict(c) -> dict:
+    out = {}
+    for name, _ in c._fields_:
+        v = getattr(c, name)
+        out[name] = list(v) if hasattr(v, "__len__") else v
+    return out
+
+
+def _apply_struct(c, d: dict) -> None:
+    for name, _ in c._fields_:
+        if name not in d:
+            continue
+        v = d[name]
+        if isinstance(v, list):
+            arr = getattr(c, name)
+            for i, x in enumerate(v):
+                arr[i] = x
+        else:
+            setattr(c, name, v)
+
+
+def _deviation(got: np.ndarray, rec: np.ndarray) -> float:
+    """Max |got - rec|; 0.0 only for a bitwise match (NaNs in the same places count as equal);
+    any non-finite difference (NaN vs number, inf - inf) is an infinite deviation."""
+    if got.size == 0 or np.array_equal(got, rec, equal_nan=True):
+        return 0.0
+    d = np.abs(got.astype(np.float64) - rec.astype(np.float64))
+    if not np.isfinite(d).all():
+        return math.inf
+    return float(d.max())
 
 
 def load(path: str) -> dict:
@@ -102,8 +144,21 @@ def replay(path: str, obs_mode: str = None, keep_obs: bool = False, device=None)
     if man["engine"] != __version__ or man["abi"] != nat.ABI_VERSION:
         raise LayoutMismatchError(f"trajectory from engine {man['engine']}/ABI {man['abi']}; this is "
                                   f"{__version__}/ABI {nat.ABI_VERSION}")
-    env = make_task(man["task"], man["num_envs"], seed=man["seed"], overrides=man["overrides"],
-                    obs_mode=obs_mode or man["obs_mode"], device=device)
+    from .cameras import CameraConfig
+    from .envs import SimConfig
+
+    cams = [CameraConfig(**{k: tuple(v) if isinstance(v, list) else v for k, v in c.items()})
+            for c in man["cameras"]] if man.get("cameras") else None
+    sim = SimConfig(**{k: tuple(v) if isinstance(v, list) else v for k, v in man["sim"].items()}) \
+        if man.get("sim") else None
+    shard = tuple(man["shard"]) if man.get("shard") else None
+    env = make_task(man["task"], man.get("global_num_envs", man["num_envs"]), seed=man["seed"],
+                    overrides=man["overrides"], obs_mode=obs_mode or man["obs_mode"], device=device, shard=shard,
+                    sim=sim, cameras=cams)
+    if env.num_envs != man["num_envs"] or env.scene.env_offset != man.get("env_offset", 0):
+        raise LayoutMismatchError("replayed shard does not match the recorded env range")
+    if man.get("c_params"):
+        _apply_struct(env.c_params, man["c_params"])  # eval mode, reset policy, seed as recorded
     if env.scene.layout_hash != man["layout_hash"]:
         raise LayoutMismatchError(f"layout {env.scene.layout_hash} != recorded {man['layout_hash']}")
     snap = {k: torch.as_tensor(v, device=env.device) for k, v in traj["initial"].items()}
@@ -120,9 +175,7 @@ def replay(path: str, obs_mode: str = None, keep_obs: bool = False, device=None)
         if not np.array_equal(r.info["success"].cpu().numpy(), traj["success"][t]):
             success_ok = False
         for k, rec in traj["states"].items():
-            got = getattr(env.scene, k).cpu().numpy()
-            d = np.abs(got.astype(np.float64) - rec[t].astype(np.float64))
-            dev[k] = max(dev[k], float(d.max()) if d.size else 0.0)
+            dev[k] = max(dev[k], _deviation(getattr(env.scene, k).cpu().numpy(), rec[t]))
         if keep_obs:
             o = r.obs
             obs_stream.append({k: v.cpu().numpy() for k, v in _flat(o).items()} if isinstance(o, dict)

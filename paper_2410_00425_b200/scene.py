@@ -164,6 +164,8 @@ class PackedModel:
             if art_name == control.robot and (not control.joints or j.name in control.joints):
                 self.ctrl[d] = n
                 self.kp[d], self.kd[d], self.flim[d] = control.kp, control.kd, control.force_limit
+                if control.mode == "base_forward_rotate":
+                    self.kp[d] = 0.0  # the base joints are velocity servos
                 n += 1
         self.action_dim = (6 if control.mode == "pd_ee_delta_pose" and n else
                            2 if control.mode == "base_forward_rotate" and n else n)

@@ -143,4 +143,6 @@ def make_task(name: str, num_envs: int, seed: int = 0, overrides=None, obs_mode:
     env.task_name = name
     env.overrides = dict(overrides or {})
     env.global_num_envs = num_envs
+    env.shard = tuple(shard) if shard is not None else None
+    env.custom_cameras = list(cameras) if cameras is not None else None
     return env

@@ -84,6 +84,35 @@ def main():
     for _ in range(1000):
         acc = acc.compose(step)
     g["chain_p"], g["chain_q"] = acc.p.copy(), acc.q.copy()
+    # free quaternion functions (pose.py:43-122) and TransformMatrixBatch (pose.py:125-164); a
+    # separate stream so the arrays above keep their values
+    r2 = np.random.default_rng(7)
+    qn_a, qn_b = g["qa_norm"], g["qb_norm"]
+    g["quat_mul"] = pose.quat_mul(qn_a, qn_b)
+    g["quat_mul_raw"] = pose.quat_mul(qa, qb)                       # unnormalized inputs too
+    g["quat_mul_bcast"] = pose.quat_mul(qn_a[:1], qn_b)             # (1,4) x (N,4)
+    g["quat_mul_nd_a"] = r2.normal(size=(3, 1, 5, 4))
+    g["quat_mul_nd_b"] = r2.normal(size=(1, 7, 5, 4))
+    g["quat_mul_nd"] = pose.quat_mul(g["quat_mul_nd_a"], g["quat_mul_nd_b"])  # (3,7,5,4)
+    g["quat_conjugate"] = pose.quat_conjugate(qa)
+    vs = r2.normal(size=(qa.shape[0], 3))
+    g["rot_v"] = vs
+    g["quat_rotate"] = pose.quat_rotate(qn_a, vs)
+    g["quat_rotate_bcast"] = pose.quat_rotate(qn_a[:1], vs)
+    g["quat_to_matrix"] = pose.quat_to_matrix(qn_a)
+    g["quat_to_matrix_raw"] = pose.quat_to_matrix(qa)
+    # matrix_to_quat on proper rotations, incl. the 180-degree / branch-boundary cases
+    rots = np.concatenate([g["quat_to_matrix"], np.stack([np.diag([1.0, -1, -1]), np.diag([-1.0, 1, -1]),
+                                                          np.diag([-1.0, -1, 1]), np.eye(3)])])
+    g["m2q_in"] = rots
+    g["matrix_to_quat"] = pose.matrix_to_quat(rots)
+    T = pose.PoseBatch(pa, qa).to_matrix()
+    U = pose.PoseBatch(pb, qb).to_matrix()
+    g["tm_a"], g["tm_b"] = T.matrices.copy(), U.matrices.copy()
+    g["tm_compose"] = T.compose(U).matrices.copy()
+    g["tm_compose_bcast"] = pose.TransformMatrixBatch(T.matrices[:1]).compose(U).matrices.copy()
+    g["tm_inverse"] = T.inverse().matrices.copy()
+    g["tm_points"] = T.transform_points(pts)
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT} ({os.path.getsize(OUT)} bytes, {len(g)} arrays)")
 

@@ -43,10 +43,12 @@ def test_partial_reset_examples(cuda):
     for t in range(5):
         env.step_random(t)
     before = env.scene.get_state()
+    obs_before = env.state_obs.clone()
     env.reset(env_mask=torch.tensor([1, 0, 0, 0], dtype=torch.bool))
     after = env.scene.get_state()
-    for k in ("qpos", "qvel", "actor_pose", "actor_vel", "goal", "elapsed"):
+    for k in env.scene.STATE_FIELDS:  # every state row, the FK cache included
         assert torch.equal(before[k][1:], after[k][1:]), k
+    assert torch.equal(env.state_obs[1:], obs_before[1:])  # re-emitted obs of untouched envs
     assert int(after["elapsed"][0]) == 0 and int(after["reset_count"][0]) == int(before["reset_count"][0]) + 1
 
 

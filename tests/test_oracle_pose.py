@@ -78,3 +78,35 @@ def test_chain_norm_drift(g):
         p, q = se3.compose(p, q, pa[:4], qa[:4])
     assert np.array_equal(bits(p), bits(g["chain_p"]))
     assert np.array_equal(bits(q), bits(g["chain_q"]))
+
+
+def nanbits(a):
+    b = bits(a).copy()
+    b[np.isnan(np.asarray(a, np.float64))] = 0x7FF8000000000000
+    return b
+
+
+def test_quaternion_functions_bit_exact(g):
+    """pose.py:43-122 free functions: the oracle restatement equals the reference's outputs."""
+    assert np.array_equal(nanbits(se3.qmul(g["qa_norm"], g["qb_norm"])), nanbits(g["quat_mul"]))
+    assert np.array_equal(nanbits(se3.qmul(g["qa_raw"], g["qb_raw"])), nanbits(g["quat_mul_raw"]))
+    assert np.array_equal(nanbits(se3.qmul(g["qa_norm"][:1], g["qb_norm"])), nanbits(g["quat_mul_bcast"]))
+    assert np.array_equal(nanbits(se3.qmul(g["quat_mul_nd_a"], g["quat_mul_nd_b"])), nanbits(g["quat_mul_nd"]))
+    assert np.array_equal(nanbits(se3.qconj(g["qa_raw"])), nanbits(g["quat_conjugate"]))
+    assert np.array_equal(nanbits(se3.qrot(g["qa_norm"], g["rot_v"])), nanbits(g["quat_rotate"]))
+    assert np.array_equal(nanbits(se3.qmat(g["qa_norm"])), nanbits(g["quat_to_matrix"]))
+    assert np.array_equal(nanbits(se3.qmat(g["qa_raw"])), nanbits(g["quat_to_matrix_raw"]))
+    assert np.array_equal(nanbits(se3.mat_to_q(g["m2q_in"])), nanbits(g["matrix_to_quat"]))
+
+
+def test_transform_matrix_batch_tolerance(g):
+    """pose.py:125-164 (matmul / einsum: BLAS summation order is unspecified) to 1e-12."""
+    a, b = g["tm_a"], g["tm_b"]
+    fin = np.isfinite(g["tm_compose"])
+    assert np.abs((a @ b)[fin] - g["tm_compose"][fin]).max() < 1e-12
+    r = np.swapaxes(a[:, :3, :3], 1, 2)
+    inv = np.tile(np.eye(4), (len(a), 1, 1))
+    inv[:, :3, :3] = r
+    inv[:, :3, 3] = -np.einsum("nij,nj->ni", r, a[:, :3, 3])
+    fin = np.isfinite(g["tm_inverse"])
+    assert np.abs(inv[fin] - g["tm_inverse"][fin]).max() < 1e-12

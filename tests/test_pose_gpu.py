@@ -226,3 +226,52 @@ def test_ref_transform_matrix_batch(P):
     assert torch.allclose(a.compose(b).matrices, want)
     eye = torch.eye(4, dtype=torch.float64, device=want.device).repeat(8, 1, 1)
     assert torch.allclose(a.inverse().matrices @ a.matrices, eye, atol=1e-12)
+
+
+# ---- free quaternion functions and TransformMatrixBatch (pose.py:43-164) on the device ----
+
+def test_quaternion_functions_bit_exact(P, pose_golden):
+    g = pose_golden
+    t = lambda k: torch.tensor(g[k]).cuda()  # noqa: E731
+    assert np.array_equal(bits(P.quat_mul(t("qa_norm"), t("qb_norm"))), bits(g["quat_mul"]))
+    assert np.array_equal(bits(P.quat_mul(g["qa_raw"], g["qb_raw"])), bits(g["quat_mul_raw"]))
+    assert np.array_equal(bits(P.quat_mul(t("qa_norm")[:1], t("qb_norm"))), bits(g["quat_mul_bcast"]))
+    nd = P.quat_mul(g["quat_mul_nd_a"], g["quat_mul_nd_b"])
+    assert tuple(nd.shape) == (3, 7, 5, 4)
+    assert np.array_equal(bits(nd), bits(g["quat_mul_nd"]))
+    assert np.array_equal(bits(P.quat_conjugate(g["qa_raw"])), bits(g["quat_conjugate"]))
+    assert np.array_equal(bits(P.quat_rotate(t("qa_norm"), t("rot_v"))), bits(g["quat_rotate"]))
+    assert np.array_equal(bits(P.quat_rotate(t("qa_norm")[:1], t("rot_v"))), bits(g["quat_rotate_bcast"]))
+    assert np.array_equal(bits(P.quat_to_matrix(t("qa_norm"))), bits(g["quat_to_matrix"]))
+    assert np.array_equal(bits(P.quat_to_matrix(g["qa_raw"])), bits(g["quat_to_matrix_raw"]))
+    assert np.array_equal(bits(P.matrix_to_quat(g["m2q_in"])), bits(g["matrix_to_quat"]))
+    from paper_2410_00425_b200.errors import DimensionError
+
+    with pytest.raises(DimensionError):
+        P.quat_mul(np.zeros((3, 4)), np.zeros((2, 4)))
+
+
+def test_transform_matrix_batch_kernels(P, pose_golden):
+    g = pose_golden
+    A = P.TransformMatrixBatch(g["tm_a"][:1024])
+    B = P.TransformMatrixBatch(g["tm_b"][:1024])
+    for got, want in ((A.compose(B).matrices, g["tm_compose"][:1024]),
+                      (P.TransformMatrixBatch(g["tm_a"][:1]).compose(B).matrices, g["tm_compose_bcast"][:1024]),
+                      (A.inverse().matrices, g["tm_inverse"][:1024]),
+                      (A.transform_points(g["pts"][:1024]), g["tm_points"][:1024])):
+        got = got.cpu().numpy()
+        assert np.abs(got - want).max() < 1e-12
+    with pytest.raises(ValueError):
+        bad = g["tm_a"][:4].copy()
+        bad[0, 0, 0] += 1e-3
+        P.TransformMatrixBatch(bad)
+
+
+def test_posebatch_is_immutable(P):
+    a = P.PoseBatch(np.zeros((4, 3)), np.tile([1.0, 0, 0, 0], (4, 1)))
+    p, q = a.numpy()
+    with pytest.raises(ValueError):
+        p[0, 0] = 1.0  # read-only host arrays, like the reference (pose.py:195-198)
+    a.p[0, 0] = 5.0  # an in-place device write is detected by the next operation
+    with pytest.raises(ValueError):
+        a.compose(a)

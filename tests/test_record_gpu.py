@@ -52,3 +52,31 @@ def test_replay_refuses_mismatched_layout(cuda, tmp_path):
     json.dump(man, open(os.path.join(path, "manifest.json"), "w"))
     with pytest.raises(LayoutMismatchError):
         record.replay(path)
+
+
+def test_replay_restores_eval_mode_sim_config_and_shard(cuda, tmp_path):
+    """The manifest carries the full step params (eval mode: no auto-reset / early termination),
+    the SimConfig and the shard, so replay re-simulates the SAME thing bitwise."""
+    from paper_2410_00425_b200 import record
+    from paper_2410_00425_b200.envs import SimConfig
+    from paper_2410_00425_b200.metrics import eval_wrapper
+    from paper_2410_00425_b200.tasks import make_task
+
+    sim = SimConfig(solver_pos_iters=6, gravity=(0.0, 0.0, -5.0))
+    env = eval_wrapper(make_task("PickCube", 8, seed=5, overrides={"max_steps": 4}, shard=(1, 2), sim=sim))
+    assert env.scene.env_offset == 4
+    path = str(tmp_path / "ev")
+    record.record(env, lambda o: torch.full((4, 3), 0.5, device=env.device), 9, path)
+    traj = record.load(path)
+    assert (traj["states"]["elapsed"][-1] == 9).all()  # eval mode: ran past the time limit
+    rep, _ = record.replay(path)
+    assert rep["bitwise"] and rep["success_match"], rep
+
+
+def test_nan_deviation_is_not_bitwise():
+    from paper_2410_00425_b200.record import _deviation
+
+    a = np.array([1.0, np.nan])
+    assert _deviation(a, a.copy()) == 0.0
+    assert _deviation(a, np.array([1.0, 2.0])) == float("inf")
+    assert _deviation(np.array([1.0, 2.0]), np.array([1.0, 2.5])) == 0.5

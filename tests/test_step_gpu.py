@@ -298,9 +298,9 @@ def test_step_host_matches_device_step(cuda):
 
 
 def test_base_forward_rotate_matches_oracle(cuda):
-    """base_forward_rotate: 2-D action (forward, rotate) -> planar
-    targets of an abstract mobile base; device == oracle within 1e-9 and the base drives along
-    its heading."""
+    """base_forward_rotate: 2-D action (forward, rotate) -> VELOCITY
+    targets of an abstract mobile base (m/s along the heading, rad/s); device == oracle within
+    1e-9, and the base drives along its heading at the commanded speed."""
     import math
 
     from oracle import engine as E
@@ -313,16 +313,17 @@ def test_base_forward_rotate_matches_oracle(cuda):
     from paper_2410_00425_b200.scene import build_batch
 
     desc = SceneDesc((ArticulationDesc("base", load_urdf(make_mobile_base_urdf())),), (), (GROUND,))
-    ctl = ControlSpec("base_forward_rotate", "base", action_scale=0.05, action_scale_rot=0.1)
+    ctl = ControlSpec("base_forward_rotate", "base", action_scale=0.5, action_scale_rot=1.0)
     scene = build_batch([desc] * 4, 0, ctl)
     env = Env(scene, cabi.TASK_NONE, [0.0] * 9, -1, 1000, 0, name="DriveBase")
     env.reset()
     assert env.action_dim == 2
     m = Model(desc)
-    drv = E.Drives(np.full(3, ctl.kp), np.full(3, ctl.kd), np.full(3, ctl.force_limit), np.zeros((4, 3)))
-    ctrl = type("C", (), {"mode": "base_forward_rotate", "dofs": [0, 1, 2], "scale": 0.05, "rot_scale": 0.1})()
+    # the base joints are velocity servos: kp = 0, kd per unit inertia
+    drv = E.Drives(np.zeros(3), np.full(3, ctl.kd), np.full(3, ctl.force_limit), np.zeros((4, 3)))
+    ctrl = type("C", (), {"mode": "base_forward_rotate", "dofs": [0, 1, 2], "scale": 0.5, "rot_scale": 1.0})()
     rng = np.random.default_rng(5)
-    for t in range(10):
+    for t in range(30):  # the 100 N force limit takes ~9 steps to reach 0.5 m/s
         q0, qd0 = env.scene.qpos.cpu().numpy(), env.scene.qvel.cpu().numpy()
         st = E.State(q0.copy(), qd0.copy(), np.zeros((4, 0, 3)), np.zeros((4, 0, 4)), np.zeros((4, 0, 3)),
                      np.zeros((4, 0, 3)), np.zeros(4, np.uint8))
@@ -332,7 +333,10 @@ def test_base_forward_rotate_matches_oracle(cuda):
         st = E.control_step(m, st, drv, ctrl, a, E.SimConfig())
         assert np.abs(env.scene.qpos.cpu().numpy() - st.q).max() < 1e-9, t
     q = env.scene.qpos.cpu().numpy()
-    assert (np.hypot(q[:, 0], q[:, 1]) > 0.005).all()  # moved forward along the heading
+    qd = env.scene.qvel.cpu().numpy()
+    assert (np.hypot(q[:, 0], q[:, 1]) > 0.15).all()  # moved forward along the heading
+    speed = np.hypot(qd[:, 0], qd[:, 1])
+    assert np.abs(speed - 0.5).max() < 0.05, speed  # tracking the 0.5 m/s velocity target
 
 
 def test_generic_width_kernel_variant(cuda):
@@ -349,3 +353,83 @@ def test_generic_width_kernel_variant(cuda):
                         "one_step_parity or trajectory_parity or ee_delta or episode_metrics"],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_graph_recaptures_after_param_changes(cuda):
+    """A captured graph bakes in BsSimParams: reset(seed=new) and eval_wrapper change them, so the
+    next replay must re-capture -- graph and eager runs stay bitwise equal through both."""
+    from paper_2410_00425_b200.metrics import eval_wrapper
+    from paper_2410_00425_b200.tasks import make_task
+
+    a = make_task("PickCube", 32, seed=9, overrides={"max_steps": 5})
+    b = make_task("PickCube", 32, seed=9, overrides={"max_steps": 5})
+    b.capture_graph()
+    for seed in (9, 123):
+        a.reset(seed=seed)
+        b.reset(seed=seed)
+        for t in range(12):  # crosses two auto-resets, which draw from the new seed's streams
+            a.step_random(t)
+            b.step_random(t)
+        for k in ("qpos", "qvel", "actor_pose", "goal", "elapsed", "reset_count"):
+            assert torch.equal(getattr(a.scene, k), getattr(b.scene, k)), (seed, k)
+    eval_wrapper(a)
+    eval_wrapper(b)
+    for t in range(8):
+        ra = a.step_random(t)
+        rb = b.step_random(t)
+        assert torch.equal(ra.terminated, rb.terminated) and not bool(rb.terminated.any())
+    assert torch.equal(a.scene.elapsed, b.scene.elapsed) and int(b.scene.elapsed.max()) > 5  # no auto-reset
+
+
+def test_host_graph_follows_eval_wrapper(cuda):
+    from paper_2410_00425_b200.metrics import eval_wrapper
+    from paper_2410_00425_b200.tasks import make_task
+
+    env = make_task("PickCube", 8, seed=2, overrides={"max_steps": 3})
+    act = np.zeros((8, 3), np.float32)
+    env.step_host(act)
+    eval_wrapper(env)
+    for _ in range(6):
+        out = env.step_host(act)
+        assert not out["terminated"].numpy().any()
+    assert int(env.scene.elapsed.min()) == 7  # never auto-reset in eval mode
+
+
+def test_capture_leaves_no_trace(cuda):
+    """Capturing (and its warmup) restores the scene state AND the outputs: the obs returned by
+    reset() still describes the current state afterwards."""
+    from paper_2410_00425_b200.tasks import make_task
+
+    env = make_task("PickCube", 16, seed=4, obs_mode="rgbd")
+    obs = env.reset(seed=4)
+    st0 = {k: v.clone() for k, v in obs["sensor_data"]["base_camera"].items()}
+    state0 = env.state_obs.clone()
+    snap = env.scene.get_state()
+    env.capture_graph()
+    env.enable_host_io()
+    torch.cuda.synchronize()
+    for k in env.scene.STATE_FIELDS:
+        assert torch.equal(getattr(env.scene, k), snap[k]), k
+    assert torch.equal(env.state_obs, state0)
+    for k, v in obs["sensor_data"]["base_camera"].items():
+        assert torch.equal(v, st0[k]), k
+
+
+def test_final_obs_is_the_pre_reset_observation(cuda):
+    """info["final_obs"]: for envs auto-reset this step, the state obs of the state the episode
+    ended in (what a learner bootstraps from on truncation) == the obs of the same run without
+    auto-reset."""
+    from paper_2410_00425_b200.metrics import eval_wrapper
+    from paper_2410_00425_b200.tasks import make_task
+
+    a = make_task("PickCube", 64, seed=5, overrides={"max_steps": 3})
+    b = eval_wrapper(make_task("PickCube", 64, seed=5, overrides={"max_steps": 3}))
+    for t in range(3):
+        ra = a.step_random(t)
+        rb = b.step_random(t)
+    # envs that reached the time limit (no early termination on the way) followed the same
+    # trajectory in both runs
+    done = ra.truncated.bool() & ~ra.terminated.bool()
+    assert int(done.sum()) >= 32
+    assert torch.equal(ra.info["final_obs"][done], rb.obs[done])
+    assert not torch.equal(ra.obs, rb.obs)  # a's obs are the reset states
