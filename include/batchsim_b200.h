@@ -297,6 +297,9 @@ typedef struct BsRenderParams {
   float* frame_scratch;        /* optional device scratch [N][C][12 S_max + 20] floats: per-frame
                                   shape -> camera transforms and camera block, computed by a
                                   parallel pre-pass (NULL: computed inside the rasterizer) */
+  uint32_t* frame_queue;       /* optional device word (ABI 8): with frame_scratch, the persistent
+                                  rasterizer CTAs pull frames from this counter (dynamic load
+                                  balance across frames of unequal cost); NULL: static stride */
 } BsRenderParams;
 
 /* FrameBatch + the fused pointcloud (A-10).  Any pointer

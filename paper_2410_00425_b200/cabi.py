@@ -59,7 +59,7 @@ class BsCameraBatch(ctypes.Structure):
 
 class BsRenderParams(ctypes.Structure):
     _fields_ = [("light_dir", F64 * 3), ("ambient", F32), ("diffuse", F32), ("background", F32 * 3),
-                ("tile", I32), ("frame_scratch", P)]
+                ("tile", I32), ("frame_scratch", P), ("frame_queue", P)]
 
 
 class BsFrameBatch(ctypes.Structure):

@@ -125,6 +125,8 @@ class Renderer:
         frames = max(N * len(g["cams"]) for g in self.groups)
         self.frame_scratch = torch.empty(frames * (12 * scene.S_max + 20), dtype=torch.float32, device=dev)
         rp.frame_scratch = self.frame_scratch.data_ptr()
+        self.frame_queue = torch.zeros(4, dtype=torch.int32, device=dev)  # dynamic frame scheduling
+        rp.frame_queue = self.frame_queue.data_ptr()
         self.c_params = rp
         self.light = L
         self.env_color = None

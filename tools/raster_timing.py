@@ -7,7 +7,8 @@ Run on a GPU box; rebuilds the library with -DBS_PHASE_TIMING (thread 0 of CTAs 
 (0, 511), (0, 1023) print clock64() deltas at each phase barrier), renders a few C3 frames
 batches and prints the mean cycles per phase.  Rebuild normally afterwards.
 
-    python tools/raster_timing.py [envs] [config] [ablate: comma list of rgb,depth,seg,pointcloud]
+    [RT_STEPS=n] python tools/raster_timing.py [envs] [config] [ablate: comma list of rgb,depth,seg,pointcloud]
+(RT_STEPS: env steps before the measured frames; later steps = the arm farther from rest)
 """
 import os
 import re
@@ -26,7 +27,8 @@ from paper_2410_00425_b200.tasks import make_task
 task = {"c3": "PickCube", "c5": "PickHetero", "c4": "OpenCabinet"}[%r]
 mode = "pointcloud" if task == "OpenCabinet" else "rgbd"
 env = make_task(task, %d, seed=0, obs_mode=mode)
-for t in range(3):
+import os
+for t in range(int(os.environ.get("RT_STEPS", "3"))):
     env.step_random(t)
     torch.cuda.synchronize()
 if %r:  # output ablation: drop some frame outputs (NULL pointers skip them)
