@@ -1182,7 +1182,26 @@ __global__ void __launch_bounds__(32) k_step(const __grid_constant__ BsModelTabl
     S.elapsed[e] = el;
     S.diverged[e] = div_out;
   }
-  if (O.obs) pack_state_obs<G>(M, P, Y, E, O.obs + (int64_t)e * O.obs_dim, O.obs_dim, Dm, Ag, l);
+  if (O.obs) {
+    if ((blockIdx.x + 1) * EPW <= S.num_envs) {
+      // every group of the warp is live: stage the EPW envs' observations (consecutive rows of
+      // O.obs) in the dead constraint-row scratch, then write them as one contiguous run --
+      // full 128-byte lines instead of EPW short segments (these are PCIe writes when the obs
+      // buffer is pinned host memory, Env.step_host)
+      float* stg = reinterpret_cast<float*>(E + Y.rows);
+      pack_state_obs<G>(M, P, Y, E, stg, O.obs_dim, Dm, Ag, l);
+      __syncwarp();
+      const int od = O.obs_dim, n = EPW * od;
+      float* dst = O.obs + (int64_t)blockIdx.x * EPW * od;
+      #pragma unroll 1
+      for (int f = lane; f < n; f += 32) {
+        const int gg = f / od;
+        dst[f] = reinterpret_cast<const float*>(smem + gg * Y.total + Y.rows)[f - gg * od];
+      }
+    } else {
+      pack_state_obs<G>(M, P, Y, E, O.obs + (int64_t)e * O.obs_dim, O.obs_dim, Dm, Ag, l);
+    }
+  }
   BS_TICK(17);
   BS_CTA_END;
 }
