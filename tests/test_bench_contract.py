@@ -52,3 +52,19 @@ def test_our_arm_contract(cuda):
     c = d["clocks"]
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(c)
     assert d["e2e"]["h2d_bytes_per_step"] == 256 * 3 * 4 and d["e2e"]["d2h_bytes_per_step"] > 0
+
+
+@pytest.mark.parametrize("config", ["c4", "c5"])
+def test_reference_arm_render_workloads(config):
+    """CPU reference arms exist for the rendering configs (BASELINE configs[3], [4]) and carry
+    the same config dict as our arm (the driver compares them), the CPU model and the sample."""
+    import importlib.util
+
+    d = run_bench("--impl", "reference", "--config", config, "--steps", "1", "--warmup", "3")
+    check_base(d)
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    assert d["config"] == bench.config_for(config, 1)
+    cb = d["cpu_baseline"]
+    assert "CPU:" in cb["sample"] and "sample of" in cb["sample"] and cb["value"] > 0
