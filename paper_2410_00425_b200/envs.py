@@ -127,6 +127,7 @@ class Env:
         self._graph_key = None
         self._host_graph = None
         self._host_graph_key = None
+        self._warmed = False
 
     # ------------------------------------------------------------------ spaces
     @property
@@ -240,7 +241,7 @@ class Env:
         """Run `launch` once eagerly so every launcher has configured its kernels (shared-memory
         opt-in, occupancy queries) before a capture, then restore EVERYTHING it wrote: the
         scene state and every output buffer -- the warmup leaves no trace."""
-        if getattr(self, "_warmed", False):
+        if self._warmed:
             return
         cur = torch.cuda.current_stream(self.device)
         snap = self.scene.get_state()                      # queued on the current stream first
@@ -259,8 +260,9 @@ class Env:
             launch()
         return g
 
-    def capture_graph(self, warmup: int = 1) -> None:
-        """Capture bs_step (+ render) on the static action buffer into a CUDA graph."""
+    def capture_graph(self) -> None:
+        """Capture bs_step (+ render) on the static action buffer into a CUDA graph (after one
+        side-effect-free eager warm-up of the launchers the first time)."""
         self._graph = self._capture(lambda: self._launch_step(self.action_buf.data_ptr()))
         self._graph_key = self._params_key()
 
@@ -270,7 +272,7 @@ class Env:
         self._graph.replay()
 
     # ------------------------------------------------------------------ host I/O path
-    def enable_host_io(self, warmup: int = 1) -> None:
+    def enable_host_io(self) -> None:
         """Capture [step reading the host actions and writing obs/reward/flags to host memory
         (zero-copy over PCIe), render, D2H of the frames] as ONE CUDA graph over pinned host
         buffers, for callers that keep actions and observations on the host (``step_host``).
