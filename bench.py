@@ -7,10 +7,11 @@ CPU path timed on the host cores.
 
 Workloads (BASELINE.json configs):
 - c2 (the headline, configs[1]): state obs, 4096 envs per GPU;
-- c3 (configs[2]): obs_mode rgb+depth (+seg), one 128x128 camera, 1024 envs per GPU;
+- c3 (configs[2]): obs_mode rgb+depth (the rasterizer also writes seg on the device), one
+  128x128 camera, 1024 envs per GPU;
 - c3_4096: the same sim+render workload at the north star's 4096 envs per GPU;
 - c4 (configs[3]): OpenCabinet, pointcloud obs from one 128x128 camera, 1024 envs per GPU;
-- c5 (configs[4]): PickHetero, 2 jittered 256x256 cameras, 1024 envs per GPU.
+- c5 (configs[4]): PickHetero, rgb+depth+seg from 2 jittered 256x256 cameras, 1024 envs per GPU.
 The default run prints the c2 line and attaches c3 and c3_4096 under "secondaries".
 
 One "step" = one env.step over every env on every GPU. That is: controller -> 2 substeps of
@@ -64,14 +65,15 @@ WORKLOADS = {
     "c2": {"task": "PickCube", "envs": 4096, "obs_mode": "state",
            "desc": "C2 PickCube-style (ARM3 + cube + ground), obs_mode=state, 4096 envs/GPU"},
     "c3": {"task": "PickCube", "envs": 1024, "obs_mode": "rgbd",
-           "desc": "C3 PickCube-style, obs_mode=rgb+depth (+seg) 1 camera 128x128, 1024 envs/GPU"},
+           "desc": "C3 PickCube-style, obs_mode=rgb+depth (seg also rendered on the device) 1 camera 128x128, "
+                   "1024 envs/GPU"},
     "c3_4096": {"task": "PickCube", "envs": 4096, "obs_mode": "rgbd",
-                "desc": "C3 at the north-star scale: PickCube-style sim+render, rgb+depth (+seg) 1 camera "
+                "desc": "C3 at the north-star scale: PickCube-style sim+render, rgb+depth (seg also rendered) 1 camera "
                         "128x128, 4096 envs/GPU"},
     "c4": {"task": "OpenCabinet", "envs": 1024, "obs_mode": "pointcloud",
            "desc": "C4 OpenCabinet (ARM3 + per-env 2-6 drawer/door cabinet), obs_mode=pointcloud 1 camera "
                    "128x128, 1024 envs/GPU"},
-    "c5": {"task": "PickHetero", "envs": 1024, "obs_mode": "rgbd",
+    "c5": {"task": "PickHetero", "envs": 1024, "obs_mode": "rgb+depth+seg",
            "desc": "C5 PickHetero (per-env object kind/size/colour, jittered cameras), rgb+depth+seg 2 cameras "
                    "256x256, 1024 envs/GPU"},
 }

@@ -12,7 +12,7 @@ from . import hostmath as hm
 from . import rng as brng
 from .errors import InputError
 
-OBS_MODES = ("state", "rgb", "depth", "rgbd", "rgb+depth", "seg", "pointcloud")
+OBS_MODES = ("state", "rgb", "depth", "rgbd", "rgb+depth", "seg", "rgb+depth+seg", "pointcloud")
 
 
 @dataclass(frozen=True)

@@ -163,10 +163,13 @@ class Renderer:
             pc = torch.cat(pcs, dim=1) if len(pcs) > 1 else pcs[0]
             segs = [f["seg"].reshape(f["seg"].shape[0], -1) for f in fr.values()]
             seg = torch.cat(segs, 1) if len(segs) > 1 else segs[0]
-            return {"pointcloud": pc, "pointcloud_mask": seg != 0, "seg": seg}
+            # fixed-shape cloud + validity mask (A-10); the seg ids stay available via frames()
+            return {"pointcloud": pc, "pointcloud_mask": seg != 0}
+        # exactly the images the obs mode names (BASELINE config 3 "rgb+depth" = rgb and depth);
+        # every image is still rendered on the device -- frames() returns them all
         keep = {"rgb": ("rgb",), "depth": ("depth",), "rgbd": ("rgb", "depth"), "rgb+depth": ("rgb", "depth"),
-                "seg": ("seg",)}[mode]
-        return {"sensor_data": {name: {k: f[k] for k in keep + ("seg",)} for name, f in fr.items()}}
+                "seg": ("seg",), "rgb+depth+seg": ("rgb", "depth", "seg")}[mode]
+        return {"sensor_data": {name: {k: f[k] for k in keep} for name, f in fr.items()}}
 
 
 def voxelize(points: torch.Tensor, cell: float, lo, dims, valid: torch.Tensor = None) -> torch.Tensor:

@@ -74,8 +74,11 @@ def test_obs_dict_and_consistency(rgbd_env):
     cam = obs["sensor_data"]["base_camera"]
     assert cam["rgb"].shape == (env.num_envs, 128, 128, 3) and cam["rgb"].dtype == torch.uint8
     assert cam["depth"].shape == (env.num_envs, 128, 128)
-    seg, depth = cam["seg"].cpu().numpy(), cam["depth"].cpu().numpy()
+    assert set(cam) == {"rgb", "depth"}  # the images obs_mode "rgbd" names
+    seg, depth = env.renderer.frames()["base_camera"]["seg"].cpu().numpy(), cam["depth"].cpu().numpy()
     assert np.array_equal(seg != 0, depth != 0)
+    full = env.renderer.observation("rgb+depth+seg")["sensor_data"]["base_camera"]
+    assert set(full) == {"rgb", "depth", "seg"}
 
 
 def test_pointcloud_matches_oracle(cuda):
@@ -190,7 +193,7 @@ def test_voxelize_and_greenscreen_match_oracle(cuda):
     with pytest.raises(Exception):
         voxelize(pc, 0.0, (0, 0, 0), (2, 2, 2))
     # green screen over real frames
-    env2 = make_task("PickCube", 2, seed=9, obs_mode="rgbd")
+    env2 = make_task("PickCube", 2, seed=9, obs_mode="rgb+depth+seg")
     cam = env2.step_random(0).obs["sensor_data"]["base_camera"]
     bg = np.random.default_rng(0).integers(0, 256, (128, 128, 3), dtype=np.uint8)
     out = composite_greenscreen(cam["rgb"], cam["seg"], bg).cpu().numpy()
