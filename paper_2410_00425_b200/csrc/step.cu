@@ -677,7 +677,12 @@ __device__ __forceinline__ void substep(const Model& M, const BsSimParams& P, co
       dir = t == 0 ? n : (t == 1 ? t1 : crs(n, t1));
     }
     R* rt = rows + (3 * c + t) * RW;
-    for (int k = 0; k < RW; k += 2) *reinterpret_cast<double2*>(rt + k) = make_double2(0.0, 0.0);
+    // the joint-rate block of J accumulates in registers (written once, with W, below); only
+    // the actor block of the row is cleared in shared memory first
+    for (int k = JI(Dm); k < RW; k += 2) *reinterpret_cast<double2*>(rt + k) = make_double2(0.0, 0.0);
+    R Jq[MD];
+#pragma unroll
+    for (int i = 0; i < MD; ++i) Jq[i] = 0.0;
     const int slots[2] = {M.p_i[pi], M.p_j[pi]};
     R Kc = 0.0;
     for (int s = 0; s < 2; ++s) {
@@ -687,7 +692,11 @@ __device__ __forceinline__ void substep(const Model& M, const BsSimParams& P, co
         for (int kk = bi; kk >= 0; kk = M.parent[kk]) {
           if (M.jtype[kk] == BS_JOINT_FIXED) continue;
           const V3<R> col = add(ld3(Sv + 6 * kk + 3), crs(ld3(Sv + 6 * kk), Pc));
-          rt[JI(M.dof[kk])] += sg * dot(dir, col);
+          const R v = sg * dot(dir, col);
+          const int d = M.dof[kk];
+#pragma unroll
+          for (int i = 0; i < MD; ++i)
+            if (i == d) Jq[i] += v;
         }
       } else if (bt == BS_BODY_ACTOR) {
         const int ub = Dm + 6 * bi;
@@ -708,11 +717,18 @@ __device__ __forceinline__ void substep(const Model& M, const BsSimParams& P, co
       }
     }
     R KA = 0.0;
-    for (int i = 0; i < D; ++i) {
-      R w = 0.0;
-      for (int k = 0; k < D; ++k) w += Minv[i * Dm + k] * rt[JI(k)];
-      rt[WI(i)] = w;
-      KA += rt[JI(i)] * w;
+#pragma unroll
+    for (int i = 0; i < MD; ++i) {
+      if (i < Dm) {
+        R w = 0.0;
+        if (i < D) {
+#pragma unroll
+          for (int k = 0; k < MD; ++k)
+            if (k < D) w += Minv[i * Dm + k] * Jq[k];
+        }
+        *reinterpret_cast<double2*>(rt + JI(i)) = make_double2(Jq[i], w);
+        KA += Jq[i] * w;
+      }
     }
     Kc = KA + Kc;
     const R tp = depth > slop ? P.beta * (depth - slop) / dt : (depth >= 0.0 ? 0.0 : depth / dt);
