@@ -281,6 +281,7 @@ class Env:
         N, A = self.num_envs, max(1, self.action_dim)
         if getattr(self, "_h_action", None) is None:
             self._h_action = torch.zeros((N, A), dtype=torch.float32).pin_memory()
+            self._h_action_np = self._h_action.numpy()  # a view of the pinned buffer
             outs = self._host_outputs()
             # the arena's tensors come back in one copy; frames (render modes) one copy each
             self._h_arena = torch.zeros(self._out_arena.numel(), dtype=torch.uint8).pin_memory()
@@ -348,18 +349,18 @@ class Env:
         call.  One graph launch and one stream synchronisation per step."""
         import numpy as np
 
-        if getattr(self, "_host_graph", None) is None:
+        if self._host_graph is None:
             self.enable_host_io()
         a = np.asarray(action, dtype=np.float32)
         if a.shape != (self.num_envs, self.action_dim):
             raise DimensionError(f"action must have shape ({self.num_envs}, {self.action_dim}), got {a.shape}")
         if self.validate_actions and not np.isfinite(a).all():
             raise InputError("non-finite action")
-        self._h_action.numpy()[:, :self.action_dim] = a
+        self._h_action_np[:, :self.action_dim] = a
         if self._host_graph_key != self._params_key():
             self.enable_host_io()
         self._host_graph.replay()
-        torch.cuda.current_stream(self.device).synchronize()
+        torch.cuda.current_stream(self.device).synchronize()  # the stream replay() launched on
         return self._h_outs
 
     def host_io_bytes(self):
