@@ -209,6 +209,24 @@ def test_c3_1024_frames_persistent_loop_bit_exact(cuda):
     assert mism <= 1e-4 * total, f"state->frames: {mism} of {total} seg pixels differ"
 
 
+def test_c3_4096_frames_north_star_scale(cuda):
+    """The north-star sim+render scale (bench.py's c3_4096 line): 4096 frames, ~28 per
+    persistent CTA pulled from the frame queue; sampled frames bit-exact."""
+    from oracle.model import Model
+    from paper_2410_00425_b200.descriptors import pickcube_desc
+    from paper_2410_00425_b200.tasks import make_task
+
+    N = 4096
+    env = make_task("PickCube", N, seed=SEED + 1, obs_mode="rgbd")
+    for t in range(2):
+        env.step_random(t)
+    torch.cuda.synchronize()
+    model = Model(pickcube_desc(env.spec))
+    lp_all, ap_all = env.scene.link_pose.cpu().numpy(), env.scene.actor_pose.cpu().numpy()
+    for e in sorted(set([0, 147, 2047, 2048, 4000, 4095] + np.random.default_rng(3).choice(N, 8).tolist())):
+        check_frame(env, e, 0, oracle_frame(env, e, 0, model, lp_all[e], ap_all[e]), f"C3@4096 frame {e}")
+
+
 # ---------------------------------------------------------------------------------- C4
 def test_c4_1024_cabinets_step_and_pointcloud(cuda):
     from oracle.model import Model
