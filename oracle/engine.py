@@ -12,7 +12,10 @@ SPEC.md:346-354 (PGS), SPEC.md:402-410 (controllers) with DESIGN.md's decisions:
           (M + diag(dt*(Kd + damping) + dt^2*Kp)) qdd
               = clamp(Kp(q* - q - dt*qd) + Kd(qd* - qd), +-limit) - damping*qd - C(q, qd)
   A-7   joint limits: clamp after integration, zero the velocity into the limit
-  A-8   free bodies: explicit gyroscopic term, q <- normalize(q + dt/2 (0,w) q)
+  A-8   free bodies: q <- normalize(q + dt/2 (0,w) q) with the (post-contact) velocity w, then
+        the world angular momentum is carried to the new orientation:
+        w' = I_w(q')^-1 I_w(q) w -- torque-free rotation conserves L = I_w w exactly
+        (SPEC.md:358), the gyroscopic effect included
   bias  normal-row target: beta*(d-slop)/dt if d > slop; 0 if 0 <= d <= slop; d/dt if d < 0
         (speculative); velocity iterations keep only the speculative part
 """
@@ -115,8 +118,7 @@ def substep(model, st: State, drv: Drives, cfg: SimConfig, want_contacts=False):
     u_q = qd + dt * qdd
     # ---- free bodies
     Iw, Iw_inv = actor_world_inertia(model, st.aq)
-    gyro = -cross(st.aw, np.einsum("baij,baj->bai", Iw, st.aw))
-    u_w = st.aw + dt * np.einsum("baij,baj->bai", Iw_inv, gyro)
+    u_w = st.aw.copy()
     u_v = st.av + dt * g
     # ---- contacts at start-of-substep positions
     SP, SQ = shape_world_poses(model, LP, LQ, st.ap, st.aq)
@@ -186,6 +188,9 @@ def substep(model, st: State, drv: Drives, cfg: SimConfig, want_contacts=False):
     if model.A:
         wq = np.concatenate([np.zeros(u_w.shape[:-1] + (1,)), u_w], -1)
         aq1 = se3.qnorm(st.aq + (0.5 * dt) * se3.qmul(wq, st.aq))
+        # carry the angular momentum to the new orientation (A-8)
+        _, Iw1_inv = actor_world_inertia(model, aq1)
+        u_w = np.einsum("baij,baj->bai", Iw1_inv, np.einsum("baij,baj->bai", Iw, u_w))
     else:
         aq1 = st.aq.copy()
     finite = (np.isfinite(q1).all(1) & np.isfinite(qd1).all(1)
@@ -247,7 +252,7 @@ def controller_targets(model, ctrl, q, action, control_freq=60):
     a = np.clip(np.asarray(action, np.float64), -1.0, 1.0)
     tgt = q.copy()
     tv = np.zeros_like(q)
-    dofs = np.asarray(ctrl.dofs)
+    dofs = np.asarray(ctrl.dofs, dtype=np.int64)
     lo, hi = model.lower[dofs], model.upper[dofs]
     if ctrl.mode == PD_JOINT_DELTA_POS:
         tgt[:, dofs] = np.clip(q[:, dofs] + a * ctrl.scale, lo, hi)

@@ -155,7 +155,8 @@ __device__ __forceinline__ int pair_maxc(int code) {
   }
 }
 
-// Actor world inertia and its inverse: R diag(I) R^T, R diag(1/I) R^T (A-8).
+// Actor world inertia and its inverse: R diag(I) R^T, R diag(1/I) R^T (A-8: contact response
+// and the angular-momentum transport of the free rotation).
 __device__ __forceinline__ void actor_inertia_f(const R* Ib, Q4<R> q, R* Iw, R* Iwi) {
   R r[9];
   quat_to_matrix(q, r);
@@ -476,9 +477,10 @@ __device__ __forceinline__ void substep(const Model& M, const BsSimParams& P, co
       const V3<R> av = ld3(E + Y.avel + 6 * a), aw = ld3(E + Y.avel + 6 * a + 3);
       R Iw[9], Iwi[9];
       actor_inertia_f(M.a_inertia + 3 * a, aq, Iw, Iwi);
-      V3<R> gyro = scl(crs(aw, m3mul(Iw, aw)), -1.0);
+      // angular velocity enters the solve unchanged: the gyroscopic effect is the momentum
+      // transport after the orientation update (phase L, A-8)
       st3(E + Y.u + Dm + 6 * a, add(av, scl(grav, dt)));
-      st3(E + Y.u + Dm + 6 * a + 3, add(aw, scl(m3mul(Iwi, gyro), dt)));
+      st3(E + Y.u + Dm + 6 * a + 3, aw);
 #pragma unroll
       for (int j = 0; j < 9; ++j) E[Y.Iwi + 9 * a + j] = Iwi[j];
     }
@@ -940,6 +942,24 @@ __device__ __forceinline__ void substep(const Model& M, const BsSimParams& P, co
       const Q4<R> wq = quat_mul(Q4<R>{0.0, uwa[a].x, uwa[a].y, uwa[a].z}, aq);
       const R h = 0.5 * dt;
       aq1[a] = qnorm_f(Q4<R>{aq.w + h * wq.w, aq.x + h * wq.x, aq.y + h * wq.y, aq.z + h * wq.z});
+      {  // carry the world angular momentum to the new orientation (A-8):
+         // w' = I_w(q')^-1 I_w(q) w = R' (I_b^-1 . (R'^T R (I_b . (R^T w))))
+        const R* Ib = M.a_inertia + 3 * a;
+        R r0[9], r1[9];
+        quat_to_matrix(aq, r0);
+        quat_to_matrix(aq1[a], r1);
+        const V3<R> w = uwa[a];
+        const V3<R> wb{r0[0] * w.x + r0[3] * w.y + r0[6] * w.z, r0[1] * w.x + r0[4] * w.y + r0[7] * w.z,
+                       r0[2] * w.x + r0[5] * w.y + r0[8] * w.z};
+        const V3<R> Lb{Ib[0] * wb.x, Ib[1] * wb.y, Ib[2] * wb.z};
+        const V3<R> L{r0[0] * Lb.x + r0[1] * Lb.y + r0[2] * Lb.z, r0[3] * Lb.x + r0[4] * Lb.y + r0[5] * Lb.z,
+                      r0[6] * Lb.x + r0[7] * Lb.y + r0[8] * Lb.z};
+        const V3<R> L1{(r1[0] * L.x + r1[3] * L.y + r1[6] * L.z) / Ib[0],
+                       (r1[1] * L.x + r1[4] * L.y + r1[7] * L.z) / Ib[1],
+                       (r1[2] * L.x + r1[5] * L.y + r1[8] * L.z) / Ib[2]};
+        uwa[a] = v3(r1[0] * L1.x + r1[1] * L1.y + r1[2] * L1.z, r1[3] * L1.x + r1[4] * L1.y + r1[5] * L1.z,
+                    r1[6] * L1.x + r1[7] * L1.y + r1[8] * L1.z);
+      }
       finite &= isfinite(ap1[a].x) && isfinite(ap1[a].y) && isfinite(ap1[a].z);
       finite &= isfinite(aq1[a].w) && isfinite(aq1[a].x) && isfinite(aq1[a].y) && isfinite(aq1[a].z);
 #pragma unroll

@@ -185,7 +185,9 @@ class Env:
             finite = torch.isfinite(a).all()
             if not bool(finite):
                 raise InputError("non-finite action")
-        if a.device != self.device or a.dtype != torch.float32 or not a.is_contiguous():
+        if a.numel() == 0:  # no controlled dofs (e.g. a scene of free bodies): any valid buffer
+            ptr = self.action_buf.data_ptr()
+        elif a.device != self.device or a.dtype != torch.float32 or not a.is_contiguous():
             self.action_buf.copy_(a, non_blocking=True)
             ptr = self.action_buf.data_ptr()
         elif self._graph is not None:

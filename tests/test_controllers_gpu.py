@@ -10,6 +10,8 @@
     of 8 OpenCabinet envs with 2-6 cabinet DOF (5-9 total) stepped 500 times equals, env by
     env, the same env simulated ALONE (its own 1-env batch: D_max = its DOF, a different
     kernel width) with the same seed and substeps, within 1e-10.
+  * Free-body momentum: an asymmetric brick tumbling in zero gravity keeps its
+    angular momentum to 1e-6 per second and its linear momentum exactly; device == oracle.
 """
 
 import numpy as np
@@ -180,3 +182,52 @@ def test_heterogeneity_equivalence_500_steps(cuda):
                 assert err <= 1e-10, (t, e, err)
                 assert (q[e, d:] == 0).all() and (qd[e, d:] == 0).all()  # padding stays zero
     print(f"heterogeneity equivalence: max |batch - solo| = {worst:.3e} over {STEPS} steps, {resets} resets")
+
+
+def test_free_body_momentum_gpu(cuda):
+    """SPEC.md:358 on the device: an asymmetric brick tumbling in zero gravity (no contacts)
+    conserves angular momentum to <= 1e-6 per second and linear momentum exactly; state ==
+    oracle within 1e-9 (A-8 momentum transport)."""
+    from oracle import engine as E
+    from oracle import se3
+    from oracle.model import Model
+    from paper_2410_00425_b200 import cabi
+    from paper_2410_00425_b200.descriptors import ActorDesc, ControlSpec, SceneDesc
+    from paper_2410_00425_b200.envs import Env, SimConfig
+    from paper_2410_00425_b200.scene import build_batch
+
+    desc = SceneDesc((), (ActorDesc("brick", "box", (0.05, 0.02, 0.01), 1000.0, (0.5, 0.5, 0.5, 1.0)),), ())
+    B = 8
+    scene = build_batch([desc] * B, 0, ControlSpec())
+    env = Env(scene, cabi.TASK_NONE, [0.0] * 9, -1, 10 ** 6, 0, sim=SimConfig(gravity=(0.0, 0.0, 0.0)),
+              auto_reset=False, name="Brick")
+    env.reset()
+    rng = np.random.default_rng(0)
+    aq = se3.qnorm(rng.normal(size=(B, 1, 4)))
+    av, aw = rng.normal(size=(B, 1, 3)), rng.normal(size=(B, 1, 3)) * 5.0
+    pose = np.concatenate([np.zeros((B, 1, 3)), aq], -1)
+    env.scene.actor_pose.copy_(torch.as_tensor(pose, device=env.device))
+    env.scene.actor_vel.copy_(torch.as_tensor(np.concatenate([av, aw], -1), device=env.device))
+    m = Model(desc)
+    st = E.State(np.zeros((B, 0)), np.zeros((B, 0)), np.zeros((B, 1, 3)), aq.copy(), av.copy(), aw.copy(),
+                 np.zeros(B, np.uint8))
+    drv = E.Drives(np.zeros(0), np.zeros(0), np.zeros(0), np.zeros((B, 0)), np.zeros((B, 0)))
+    cfg = E.SimConfig(gravity=(0.0, 0.0, 0.0))
+    I_b = np.asarray(m.actor_inertia[0])
+
+    def ang_mom(q, w):
+        R = se3.qmat(q)
+        return np.einsum("bij,j,bkj,bk->bi", R, I_b, R, w)
+
+    L0 = ang_mom(aq[:, 0], aw[:, 0])
+    act = torch.zeros((B, 0), device=env.device)
+    for t in range(60):  # 1 s of 120 Hz substeps
+        env.step(act)
+        st = E.control_step(m, st, drv, type("C", (), {"mode": "pd_joint_pos", "dofs": [], "scale": 1.0})(),
+                            np.zeros((B, 0)), cfg)
+    p = env.scene.actor_pose.cpu().numpy()[:, 0]
+    v = env.scene.actor_vel.cpu().numpy()[:, 0]
+    assert np.abs(p[:, 3:] - st.aq[:, 0]).max() <= 1e-9 and np.abs(v[:, 3:] - st.aw[:, 0]).max() <= 1e-9
+    rel = np.linalg.norm(ang_mom(p[:, 3:], v[:, 3:]) - L0, axis=-1) / np.linalg.norm(L0, axis=-1)
+    assert rel.max() <= 1e-6, rel.max()
+    assert np.array_equal(v[:, :3], av[:, 0])
