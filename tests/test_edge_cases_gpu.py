@@ -76,3 +76,23 @@ def test_bad_action_shapes_and_values(cuda):
         env.step_host(np.full((2, 3), np.inf, np.float32))
     with pytest.raises(DimensionError):
         env.step_host(np.zeros((2, 4), np.float32))
+
+
+def test_time_limit_and_early_termination_examples(cuda):
+    """with no early termination, truncated is true exactly at step T; an env in
+    its success state with early termination on is terminated that very step."""
+    from paper_2410_00425_b200.metrics import eval_wrapper
+    from paper_2410_00425_b200.tasks import make_task
+
+    T = 5
+    env = eval_wrapper(make_task("PickCube", 4, seed=1, overrides={"max_steps": T}))
+    for t in range(1, T + 2):
+        r = env.step(torch.zeros((4, 3), device=env.device))
+        assert bool(r.truncated.all()) == (t >= T), t
+        assert not bool(r.terminated.any())
+    env = make_task("PickCube", 4, seed=1)
+    s = env.scene
+    s.actor_pose[1, 0, :2] = s.goal[1, :2]  # env 1 starts on its goal: success on the next step
+    r = env.step(torch.zeros((4, 3), device=env.device))
+    assert bool(r.info["success"][1]) and bool(r.terminated[1])
+    assert not bool(r.terminated[0])
