@@ -95,4 +95,5 @@ def test_time_limit_and_early_termination_examples(cuda):
     s.actor_pose[1, 0, :2] = s.goal[1, :2]  # env 1 starts on its goal: success on the next step
     r = env.step(torch.zeros((4, 3), device=env.device))
     assert bool(r.info["success"][1]) and bool(r.terminated[1])
-    assert not bool(r.terminated[0])
+    done = (r.info["success"] | r.info["fail"]).bool()
+    assert torch.equal(r.terminated.bool(), done)
