@@ -12,7 +12,8 @@ Workloads (BASELINE.json configs):
 - c3_4096: the same sim+render workload at the north star's 4096 envs per GPU;
 - c4 (configs[3]): OpenCabinet, pointcloud obs from one 128x128 camera, 1024 envs per GPU;
 - c5 (configs[4]): PickHetero, rgb+depth+seg from 2 jittered 256x256 cameras, 1024 envs per GPU.
-The default run prints the c2 line and attaches c3 and c3_4096 under "secondaries".
+The default run prints the c2 line and attaches c3, c3_4096, c4 and c5 under "secondaries" (every
+BASELINE config in one line).
 
 One "step" = one env.step over every env on every GPU. That is: controller -> 2 substeps of
 dynamics, contacts and PGS -> FK -> reward/termination -> state obs -> auto-reset, plus the
@@ -601,7 +602,7 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", choices=sorted(WORKLOADS), default="c2")
-    ap.add_argument("--secondary", default="c3,c3_4096",
+    ap.add_argument("--secondary", default="c3,c3_4096,c4,c5",
                     help="comma list of extra workloads measured after the headline ('' = none)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
