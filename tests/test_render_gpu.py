@@ -199,3 +199,33 @@ def test_voxelize_and_greenscreen_match_oracle(cuda):
     out = composite_greenscreen(cam["rgb"], cam["seg"], bg).cpu().numpy()
     want = raster.composite_greenscreen(cam["rgb"].cpu().numpy(), cam["seg"].cpu().numpy(), bg)
     assert np.array_equal(out, want)
+
+
+def test_pointcloud_reprojection_round_trip(cuda):
+    """SPEC.md:500 / acceptance criterion 6: every valid point of the device pointcloud
+    re-projects through the same camera onto its own pixel centre within 0.5 px."""
+    from paper_2410_00425_b200.tasks import make_task
+
+    env = make_task("OpenCabinet", 6, seed=3, obs_mode="pointcloud")
+    env.step_random(0)
+    torch.cuda.synchronize()
+    g = env.renderer.groups[0]
+    W, H = g["w"], g["h"]
+    pc = g["pc"][:, 0].cpu().numpy().astype(np.float64)
+    valid = (g["seg"][:, 0].cpu().numpy().view(np.uint16) != 0).reshape(len(pc), -1)
+    pose, intr = g["pose"][:, 0].cpu().numpy(), g["intr"][:, 0].cpu().numpy().astype(np.float64)
+    vv, uu = np.meshgrid(np.arange(H), np.arange(W), indexing="ij")
+    for e in range(len(pc)):
+        w, x, y, z = pose[e, 3:]
+        R = np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
+                      [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
+                      [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])
+        cam = (pc[e, :, :3] - pose[e, :3]) @ R  # world -> camera: R^T (p - t), row-vector form
+        fx, fy, cx, cy = intr[e]
+        u = fx * cam[:, 0] / cam[:, 2] + cx
+        v = fy * cam[:, 1] / cam[:, 2] + cy
+        m = valid[e]
+        assert m.sum() > 100
+        assert np.abs(u[m] - (uu.ravel()[m] + 0.5)).max() <= 0.5
+        assert np.abs(v[m] - (vv.ravel()[m] + 0.5)).max() <= 0.5
+        assert (pc[e][~m] == 0).all()
