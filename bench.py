@@ -406,12 +406,12 @@ def run_reference(args):
 
 # ------------------------------------------------------------------------------ GPU path
 def measure(env, steps, warmup, flush, dist, local, seed_step=0):
-    from paper_2410_00425_b200 import dist as bdist
-
     """Device timing of `steps` env steps: the steps' synthetic actions are generated into HBM
     before the timed region (Philox, the same stream step_random uses); per step, flush L2
     (untimed), then events around the fused step and the render."""
     import torch
+
+    from paper_2410_00425_b200 import dist as bdist
 
     stream = torch.cuda.current_stream(env.device)
     for k in range(warmup):
@@ -441,21 +441,21 @@ def measure(env, steps, warmup, flush, dist, local, seed_step=0):
     t = torch.tensor([sum(e[0].elapsed_time(e[3]) for e in ev), sum(e[1].elapsed_time(e[2]) for e in ev),
                       sum(e[2].elapsed_time(e[3]) for e in ev)], dtype=torch.float64, device=env.device)
     bdist.max_over_ranks(t)  # the job is as slow as its slowest rank
-    # k_step, and per camera group k_frame_setup + k_render
+    # k_step, and per camera group k_frame_setup + k_render (our kernels in the timed region)
     launches = 1 + (2 * len(env.renderer.groups) if env.renderer is not None else 0)
     return {"step_ms": float(t[0]), "sim_ms": float(t[1]), "render_ms": float(t[2]), "clocks": clk.summary(),
             "launches": launches * steps}
 
 
 def measure_e2e(env, steps, dist, seed):
-    from paper_2410_00425_b200 import dist as bdist
-
     """The public API with host buffers: Env.step_host(host action) -- one CUDA graph in which
     the step kernel reads the pinned host actions and writes obs / reward / flags to pinned host
     memory over PCIe (zero-copy), plus the render and the D2H copies of the frames -- then a
     stream synchronisation, every step."""
     import numpy as np
     import torch
+
+    from paper_2410_00425_b200 import dist as bdist
 
     N = env.num_envs
     rng = np.random.default_rng(seed)
@@ -491,7 +491,6 @@ def run_workload(name, steps, warmup, world, rank, local, dist, flush, seed, e2e
     import torch
 
     from paper_2410_00425_b200 import dist as bdist
-
     from paper_2410_00425_b200.tasks import make_task
 
     wl = WORKLOADS[name]
