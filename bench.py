@@ -20,14 +20,15 @@ dynamics, contacts and PGS -> FK -> reward/termination -> state obs -> auto-rese
 render for camera workloads. Steps are fed by uniform random actions.
 
 Timing rules:
-- `value`: device time (CUDA events on the launching stream) summed over K steps, with inputs
+- `value`: device time (CUDA events on the launching stream, first to last of each step) summed over K steps, with inputs
   resident in HBM. The L2 is flushed (a 256 MiB write) BEFORE every timed step, outside the
   events, so every step starts cold. The max is taken over ranks; the figure is whole-job
   env-steps/s.
 - `e2e`: the public API with host buffers (`Env.step_host(host action)`): actions read from
   pinned host memory and obs/reward/flags (+ frames) written back every step; wall clock,
   synchronised, max over ranks.
-- `roofline`: the dominant kernel alone (events around its launch). Algorithmic bytes per
+- `roofline`: the dominant kernel alone (the event pair around its launches inside the timed
+  steps). Algorithmic bytes per
   env-step / duration, against
   MEASURED_PEAKS.json hbm_gbs.
 - `cpu_baseline` (rank 0, N=1 only): the oracle (CPU restatement of the reference path,
@@ -408,7 +409,10 @@ def run_reference(args):
 def measure(env, steps, warmup, flush, dist, local, seed_step=0):
     """Device timing of `steps` env steps: the steps' synthetic actions are generated into HBM
     before the timed region (Philox, the same stream step_random uses); per step, flush L2
-    (untimed), then events around the fused step and the render."""
+    (untimed), then CUDA events on the launching stream: one before the fused step kernel, one
+    after it, and -- render workloads only -- one after the render launches.  The step interval
+    is first event -> last event; the kernel intervals are the consecutive pairs.  (An extra
+    event record before a kernel costs ~2.5 us of device time per step, so there is none.)"""
     import torch
 
     from paper_2410_00425_b200 import dist as bdist
@@ -421,7 +425,8 @@ def measure(env, steps, warmup, flush, dist, local, seed_step=0):
         env.random_actions(seed_step + warmup + k)
         acts[k].copy_(env.action_buf)
     torch.cuda.synchronize()
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
+    render = env.renderer is not None
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3 if render else 2)] for _ in range(steps)]
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
@@ -429,20 +434,21 @@ def measure(env, steps, warmup, flush, dist, local, seed_step=0):
         for k in range(steps):
             flush.zero_()                      # cold L2 before every timed step (not timed)
             ev[k][0].record(stream)
-            ev[k][1].record(stream)
             env._launch_sim(acts[k].data_ptr())
-            ev[k][2].record(stream)
-            env._render()
-            ev[k][3].record(stream)
+            ev[k][1].record(stream)
+            if render:
+                env._render()
+                ev[k][2].record(stream)
         torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
-    t = torch.tensor([sum(e[0].elapsed_time(e[3]) for e in ev), sum(e[1].elapsed_time(e[2]) for e in ev),
-                      sum(e[2].elapsed_time(e[3]) for e in ev)], dtype=torch.float64, device=env.device)
+    t = torch.tensor([sum(e[0].elapsed_time(e[-1]) for e in ev), sum(e[0].elapsed_time(e[1]) for e in ev),
+                      sum(e[1].elapsed_time(e[2]) for e in ev) if render else 0.0], dtype=torch.float64,
+                     device=env.device)
     bdist.max_over_ranks(t)  # the job is as slow as its slowest rank
     # k_step, and per camera group k_frame_setup + k_render (our kernels in the timed region)
-    launches = 1 + (2 * len(env.renderer.groups) if env.renderer is not None else 0)
+    launches = 1 + (2 * len(env.renderer.groups) if render else 0)
     return {"step_ms": float(t[0]), "sim_ms": float(t[1]), "render_ms": float(t[2]), "clocks": clk.summary(),
             "launches": launches * steps}
 
