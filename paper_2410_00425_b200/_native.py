@@ -15,7 +15,8 @@ import re
 from .errors import raise_for_status
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libbatchsim_b200.so")
+# BS_LIB_PATH: an alternative in-tree build of the same library (A/B timing scripts only)
+LIB_PATH = os.environ.get("BS_LIB_PATH") or os.path.join(HERE, "_lib", "libbatchsim_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "batchsim_b200.h")
 ABI_VERSION = 8
 
