@@ -17,6 +17,7 @@ import math
 from dataclasses import dataclass
 from typing import NamedTuple
 
+import numpy as np
 import torch
 
 from . import _native as nat
@@ -284,6 +285,7 @@ class Env:
         if getattr(self, "_h_action", None) is None:
             self._h_action = torch.zeros((N, A), dtype=torch.float32).pin_memory()
             self._h_action_np = self._h_action.numpy()  # a view of the pinned buffer
+            self._h_zeros = np.zeros(N * A, dtype=np.float32)
             outs = self._host_outputs()
             # the arena's tensors come back in one copy; frames (render modes) one copy each
             self._h_arena = torch.zeros(self._out_arena.numel(), dtype=torch.uint8).pin_memory()
@@ -349,16 +351,16 @@ class Env:
         """Host-resident step: `action` (N, D) array-like on the host -> dict of pinned host
         tensors (obs..., reward, terminated, truncated, success, fail), valid until the next
         call.  One graph launch and one stream synchronisation per step."""
-        import numpy as np
-
         if self._host_graph is None:
             self.enable_host_io()
         a = np.asarray(action, dtype=np.float32)
         if a.shape != (self.num_envs, self.action_dim):
             raise DimensionError(f"action must have shape ({self.num_envs}, {self.action_dim}), got {a.shape}")
-        if self.validate_actions and not np.isfinite(a).all():
-            raise InputError("non-finite action")
         self._h_action_np[:, :self.action_dim] = a
+        # exact non-finite test in one BLAS pass: x * 0 is 0 for every finite x and NaN for
+        # inf / NaN, so the dot with zeros is finite iff every action is (no overflow possible)
+        if self.validate_actions and not np.isfinite(np.dot(self._h_action_np.reshape(-1), self._h_zeros)):
+            raise InputError("non-finite action")
         if self._host_graph_key != self._params_key():
             self.enable_host_io()
         self._host_graph.replay()

@@ -76,6 +76,19 @@ def test_bad_action_shapes_and_values(cuda):
         env.step_host(np.full((2, 3), np.inf, np.float32))
     with pytest.raises(DimensionError):
         env.step_host(np.zeros((2, 4), np.float32))
+    # one non-finite entry among finite ones is rejected before anything is launched; the
+    # largest finite floats are not (the host check is a dot with zeros: no overflow)
+    before = env.scene.get_state()
+    for bad in (np.nan, -np.inf, np.inf):
+        a = np.zeros((2, 3), np.float32)
+        a[1, 2] = bad
+        with pytest.raises(InputError):
+            env.step_host(a)
+    after = env.scene.get_state()
+    for k in env.scene.STATE_FIELDS:
+        assert torch.equal(before[k], after[k]), k
+    env.step_host(np.full((2, 3), np.finfo(np.float32).max, np.float32))
+    env.step_host(np.full((2, 3), -np.finfo(np.float32).max, np.float32))
 
 
 def test_time_limit_and_early_termination_examples(cuda):

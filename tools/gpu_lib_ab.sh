@@ -12,7 +12,7 @@ for rep in 1 2; do
 import json, sys
 try:
     d = json.loads(open(sys.argv[2]).read().strip().splitlines()[-1])
-    print(sys.argv[1], {k: round(v["us_per_launch"], 1) for k, v in d["roofline"]["kernels"].items()}, "value=%.4g" % d["value"])
+    print(sys.argv[1], {k: round(v["us_per_launch"], 1) for k, v in d["roofline"]["kernels"].items()}, "value=%.4g" % d["value"], "e2e=%.4g" % (d.get("e2e") or {}).get("value", 0))
 except Exception as e:
     print(sys.argv[1], "failed", e)
 PY
