@@ -110,8 +110,9 @@ def test_random_views_all_tiles_bit_exact(cuda, res, obs_mode):
 @pytest.mark.parametrize("caps,obs_mode", [("4,16", "rgbd"), ("1,1", "pointcloud"), ("256,64", "rgbd")])
 def test_overflow_paths_bit_exact(cuda, caps, obs_mode):
     """With the big-record and span capacities lowered (BS_RENDER_CAPS, a test knob read once per
-    process), triangles past the record capacity are drawn in-thread at classification and
-    spans past the list capacity are drawn in-lane -- frames must still equal the oracle."""
+    process), triangles past the record capacity are set up in later rounds (at most the record
+    capacity per round) and row items run in windows of the span capacity -- "1,1" makes every
+    big triangle its own round and every row its own window.  Frames must equal the oracle."""
     import os
     import subprocess
     import sys
