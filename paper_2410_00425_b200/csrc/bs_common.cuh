@@ -35,7 +35,7 @@ static inline int launch_status() {
 constexpr int kMaxDevices = 64;
 struct LaunchCache {
   std::mutex mu;
-  size_t optin[8][kMaxDevices] = {};
+  size_t optin[16][kMaxDevices] = {};
 };
 static inline LaunchCache& launch_cache() {
   static LaunchCache c;

@@ -1330,8 +1330,12 @@ static int launch(const BsModelTables& T, const BsEnvState& S, const BsStepOutpu
 }
 
 typedef Cfg<8, 3, 1, true, 1> CfgPick;  // exactly ARM3 + one free actor (PickCube, PickHetero): static widths
+typedef Cfg<16, 3, 1, true, 5> CfgPick16;  // the same with 16 lanes per env (small batches: idle SMs)
+typedef Cfg<32, 3, 1, true, 6> CfgPick32;  // the same with a whole warp per env
 typedef Cfg<8, 4, 1, false, 2> CfgSmall;    // PickCube-style: D <= 4, one free actor
 typedef Cfg<8, 12, 1, false, 3> CfgArt;     // articulated objects (arm + cabinet): D <= 12, <= 1 actor
+typedef Cfg<16, 12, 1, false, 7> CfgArt16;
+typedef Cfg<32, 12, 1, false, 8> CfgArt32;
 typedef Cfg<8, 12, 4, false, 4> CfgLarge;   // general scenes: D <= 12, <= 4 actors
 
 }  // namespace step
@@ -1367,10 +1371,36 @@ int bs_step(const BsModelTables* T, const BsEnvState* S, const BsStepOutputs* O,
     const char* v = getenv("BS_STEP_GENERIC");  // tests: force the runtime-width variants
     return v && atoi(v) != 0;
   }();
-  if (!generic && T->D_max == CfgPick::MD && T->A_max == CfgPick::MA && T->A_dyn == CfgPick::MA)
+  // Lanes per env (PickCube-style and articulated variants).  A launch lasts as long as its
+  // slowest env's dependency chain, and small batches leave most SMSPs idle: there, 16 or 32
+  // lanes per env shorten the lane-parallel phases (pairs, rows, links) at no cost in
+  // residency.  Large batches keep 8 lanes (all 4096 PickCube envs resident in one wave).
+  // Measured on one B200 (tools/ab_g.sh): 512 envs 62 -> 55 us (G 32), 1024 envs 64 -> 60 us
+  // (G 16/32), C4 cabinets 127 -> 107 us (G 16), 4096 envs 72 us (G 8; G 16: 112 us).
+  // BS_STEP_G = 8 / 16 / 32 forces a variant (tests run the parity cases on each).
+  static const int gforce = [] {
+    const char* v = getenv("BS_STEP_G");
+    const int g = v ? atoi(v) : 0;
+    return g == 8 || g == 16 || g == 32 ? g : 0;
+  }();
+  auto lanes = [&](int n) {
+    if (gforce) return gforce;
+    const long budget = 112L * bs::sm_count();  // env-lanes per launch that keep the step one short wave
+    return (long)n * 32 <= budget ? 32 : ((long)n * 16 <= budget ? 16 : 8);
+  };
+  if (!generic && T->D_max == CfgPick::MD && T->A_max == CfgPick::MA && T->A_dyn == CfgPick::MA) {
+    const int g = lanes(S->num_envs);
+    if (g == 32) return launch<CfgPick32>(*T, *S, *O, *P, action, st);
+    if (g == 16) return launch<CfgPick16>(*T, *S, *O, *P, action, st);
     return launch<CfgPick>(*T, *S, *O, *P, action, st);
+  }
   if (T->D_max <= CfgSmall::MD && T->A_max <= CfgSmall::MA) return launch<CfgSmall>(*T, *S, *O, *P, action, st);
-  if (T->D_max <= CfgArt::MD && T->A_max <= CfgArt::MA) return launch<CfgArt>(*T, *S, *O, *P, action, st);
+  if (T->D_max <= CfgArt::MD && T->A_max <= CfgArt::MA) {
+    const int g = lanes(S->num_envs);
+    if (g == 32) return launch<CfgArt32>(*T, *S, *O, *P, action, st);
+    if (g == 16) return launch<CfgArt16>(*T, *S, *O, *P, action, st);
+    return launch<CfgArt>(*T, *S, *O, *P, action, st);
+  }
   if (T->D_max <= CfgLarge::MD && T->A_max <= CfgLarge::MA) return launch<CfgLarge>(*T, *S, *O, *P, action, st);
   return BS_ERR_UNSUPPORTED;
 }

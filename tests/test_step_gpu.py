@@ -355,6 +355,26 @@ def test_generic_width_kernel_variant(cuda):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
+@pytest.mark.parametrize("lanes", [8, 16, 32])
+def test_lane_count_variants(cuda, lanes):
+    """bs_step picks 8, 16 or 32 lanes per env from the batch size (small batches get more lanes
+    per env); force each variant (BS_STEP_G) and rerun the parity tests of this module and the
+    cabinet (articulated-variant) tests on it."""
+    import os
+    import subprocess
+    import sys
+
+    if os.environ.get("BS_STEP_G") or os.environ.get("BS_STEP_GENERIC"):
+        pytest.skip("already running a forced variant")
+    env = dict(os.environ, BS_STEP_G=str(lanes))
+    here = os.path.dirname(__file__)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", __file__,
+                        os.path.join(here, "test_cabinet_gpu.py"), "-k",
+                        "one_step_parity or trajectory_parity or ee_delta or episode_metrics or cabinet"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
 def test_graph_recaptures_after_param_changes(cuda):
     """A captured graph bakes in BsSimParams: reset(seed=new) and eval_wrapper change them, so the
     next replay must re-capture -- graph and eager runs stay bitwise equal through both."""
