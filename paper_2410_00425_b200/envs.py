@@ -308,9 +308,13 @@ class Env:
                      ctypes.byref(self._c_out_host), ctypes.byref(self.c_params), self._h_action.data_ptr(),
                      nat.stream_handle())
             self._render()
+            # observation entries derived on the device (the pointcloud validity mask, multi-camera
+            # concatenations) are recomputed inside the captured region, not read from the
+            # tensors of the capture-time call
+            cur = self._flatten_obs(self._obs()) if self.renderer is not None else {}
             for k, v in self._h_dev_outs.items():
                 if k not in self._h_in_arena:
-                    self._h_outs[k].copy_(v, non_blocking=True)
+                    self._h_outs[k].copy_(cur.get(k, v), non_blocking=True)
 
         self._warm_launchers(lambda: self._launch_step(self.action_buf.data_ptr()))
         self._host_graph = self._capture(launch)
@@ -331,20 +335,26 @@ class Env:
             n += nb
         return out
 
+    @staticmethod
+    def _flatten_obs(o) -> dict:
+        """{"obs/<path>": tensor} of a (nested) observation dict; a bare tensor is "obs"."""
+        if not isinstance(o, dict):
+            return {"obs": o}
+        out = {}
+
+        def walk(d, prefix=""):
+            for k, v in d.items():
+                if isinstance(v, dict):
+                    walk(v, prefix + k + "/")
+                else:
+                    out["obs/" + prefix + k] = v
+        walk(o)
+        return out
+
     def _host_outputs(self) -> dict:
         out = {"reward": self.reward, "terminated": self.terminated, "truncated": self.truncated,
                "success": self.success, "fail": self.fail}
-        o = self._obs()
-        if isinstance(o, dict):
-            def walk(d, prefix=""):
-                for k, v in d.items():
-                    if isinstance(v, dict):
-                        walk(v, prefix + k + "/")
-                    else:
-                        out["obs/" + prefix + k] = v
-            walk(o)
-        else:
-            out["obs"] = o
+        out.update(self._flatten_obs(self._obs()))
         return out
 
     def step_host(self, action):

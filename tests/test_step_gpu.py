@@ -275,26 +275,33 @@ def test_episode_metrics_match_oracle(cuda):
     assert int(stats.sums[0]) == episodes
 
 
-def test_step_host_matches_device_step(cuda):
+@pytest.mark.parametrize("task,obs_mode,over", [
+    ("PickCube", "rgbd", None),
+    ("PickCube", "rgb+depth+seg", None),
+    ("PickCube", "pointcloud", None),
+    ("PickHetero", "rgb+depth+seg", {"camera_res": 64}),  # two cameras in one group
+])
+def test_step_host_matches_device_step(cuda, task, obs_mode, over):
     """Env.step_host (one graph: step with zero-copy host actions and obs/reward/flags, render, D2H
-    frames) == Env.step, several steps in a row (auto-resets included)."""
+    of the images and of the device-derived entries such as the pointcloud mask) == Env.step,
+    every returned array bitwise, several steps in a row (auto-resets included)."""
+    from paper_2410_00425_b200.envs import Env
     from paper_2410_00425_b200.tasks import make_task
 
-    a = make_task("PickCube", 8, seed=17, obs_mode="rgbd")
-    b = make_task("PickCube", 8, seed=17, obs_mode="rgbd")
+    a = make_task(task, 8, seed=17, obs_mode=obs_mode, overrides=over)
+    b = make_task(task, 8, seed=17, obs_mode=obs_mode, overrides=over)
     rng = np.random.default_rng(2)
     for t in range(6):
-        act = rng.uniform(-1, 1, (8, 3)).astype(np.float32)
+        act = rng.uniform(-1, 1, (8, a.action_dim)).astype(np.float32)
         ra = a.step(torch.as_tensor(act, device=a.device))
         hb = b.step_host(act)
-        assert np.array_equal(ra.reward.cpu().numpy(), hb["reward"].numpy())
-        for k in ("terminated", "truncated", "success", "fail"):
-            assert np.array_equal(getattr(a, k).cpu().numpy(), hb[k].numpy()), k
-        assert np.array_equal(ra.obs["state"].cpu().numpy(), hb["obs/state"].numpy())
-        assert np.array_equal(ra.obs["sensor_data"]["base_camera"]["rgb"].cpu().numpy(),
-                              hb["obs/sensor_data/base_camera/rgb"].numpy())
+        dev = {"reward": ra.reward, **{k: getattr(a, k) for k in ("terminated", "truncated", "success", "fail")}}
+        dev.update(Env._flatten_obs(ra.obs))
+        assert set(dev) == set(hb), (sorted(dev), sorted(hb))
+        for k, v in dev.items():
+            assert np.array_equal(v.cpu().numpy(), hb[k].numpy()), (t, k)
     h2d, d2h = b.host_io_bytes()
-    assert h2d == 8 * 3 * 4 and d2h > 8 * 128 * 128 * 3
+    assert h2d == 8 * a.action_dim * 4 and d2h > 8 * 64 * 64
 
 
 def test_base_forward_rotate_matches_oracle(cuda):
