@@ -34,7 +34,7 @@ extern "C" {
 #define BS_ERR_UNSUPPORTED 6 /* ModelError      (errors.py:40) */
 
 /* ABI version: bumped whenever a signature or a struct layout below changes. */
-#define BS_ABI_VERSION 8
+#define BS_ABI_VERSION 9
 int bs_abi_version(void);
 
 /* Bind the library's CUDA runtime to `device` (call once per process/thread before use;
@@ -276,6 +276,8 @@ typedef struct BsMeshTables {
   const int32_t* vert_shape;   /* [M][V_max] shape slot of the vertex */
   const int32_t* tris;         /* [M][T_max][3] */
   const int32_t* tri_shape;    /* [M][T_max] shape slot of the triangle */
+  const int32_t* tri_packed;   /* [M][T_max][4] i0, i1, i2, shape slot: the same triangles as one
+                                  16-byte record each (may be NULL: tris + tri_shape are read; ABI 9) */
 } BsMeshTables;
 
 /* CameraConfig: one group of cameras sharing a resolution.  OpenCV axes

@@ -18,7 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # BS_LIB_PATH: an alternative in-tree build of the same library (A/B timing scripts only)
 LIB_PATH = os.environ.get("BS_LIB_PATH") or os.path.join(HERE, "_lib", "libbatchsim_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "batchsim_b200.h")
-ABI_VERSION = 8
+ABI_VERSION = 9
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64

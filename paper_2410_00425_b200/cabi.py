@@ -49,7 +49,7 @@ F32 = ctypes.c_float
 
 class BsMeshTables(ctypes.Structure):
     _fields_ = [("num_models", I32), ("V_max", I32), ("T_max", I32)] + [
-        (n, P) for n in ("n_verts", "n_tris", "verts", "vert_shape", "tris", "tri_shape")]
+        (n, P) for n in ("n_verts", "n_tris", "verts", "vert_shape", "tris", "tri_shape", "tri_packed")]
 
 
 class BsCameraBatch(ctypes.Structure):

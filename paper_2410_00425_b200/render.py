@@ -46,7 +46,11 @@ class MeshTables:
             nv[i], nt[i] = len(p["verts"]), len(p["tris"])
             verts[i, :nv[i]], vsh[i, :nv[i]] = p["verts"], p["vert_shape"]
             tris[i, :nt[i]], tsh[i, :nt[i]] = p["tris"], p["tri_shape"]
-        self.host = dict(verts=verts, vert_shape=vsh, tris=tris, tri_shape=tsh, n_verts=nv, n_tris=nt)
+        # the same triangles as one 16-byte record each (i0, i1, i2, shape slot): the rasterizer's
+        # per-frame triangle pass reads one record per triangle (ABI 9)
+        packed = np.concatenate([tris, tsh[..., None]], axis=-1).astype(np.int32)
+        self.host = dict(verts=verts, vert_shape=vsh, tris=tris, tri_shape=tsh, tri_packed=packed, n_verts=nv,
+                         n_tris=nt)
         self.per_model = per
         dev = scene.device
         self.t = {k: torch.as_tensor(v, device=dev) for k, v in self.host.items()}

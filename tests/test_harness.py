@@ -122,3 +122,14 @@ def test_run_bench_on_gpu(cuda, tmp_path):
     H.emit_csv(res, tmp_path / "g.csv")
     H.emit_plotdata(res, tmp_path / "g.json")
     assert len(H.parse_csv(tmp_path / "g.csv")) == len(res)
+
+
+@pytest.mark.gpu
+def test_cartpole_fps_scaling_acceptance(cuda):
+    """Acceptance criterion 9: CartpoleBalance state-only aggregate fps at 256
+    envs >= 8x the fps at 4 envs, through the harness at its default 1000 timed steps (on the
+    GPU one launch steps every env, so the ratio approaches the env-count ratio)."""
+    res = H.run_bench("CartpoleBalance", [4, 256], warmup_steps=20)
+    assert all(r.fps > 0 and not r.error for r in res), res
+    assert res[0].steps == 1000
+    assert res[1].fps >= 8 * res[0].fps, (res[0].fps, res[1].fps)
