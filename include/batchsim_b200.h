@@ -324,6 +324,14 @@ int bs_render(const BsModelTables* tables, const BsEnvState* state, const BsMesh
               const BsFrameBatch* out, void* stream);
 
 
+/* Env.step_host's host-side step (ABI 9): copy `n` floats of actions from host memory `src`
+ * into the pinned host buffer `dst` that a captured step graph reads (zero-copy), reject the step
+ * with BS_ERR_INPUT before anything is launched when check != 0 and an action is not finite,
+ * then launch `graph_exec` (a cudaGraphExec_t) on `stream` and synchronise the stream.  Replaces
+ * the per-step host work of the reference's env.step(action) call path for
+ * callers that keep actions and observations on the host. */
+int bs_host_step(const float* src, float* dst, int64_t n, int32_t check, void* graph_exec, void* stream);
+
 /* voxelize(points, cell, bounds): occupancy grid [batches][nx][ny][nz] u8 of
  * points (xyz at the start of each `point_stride`-float record, e.g. the fused pointcloud with
  * stride 6), cell index = floor((p - lo) / cell) per axis in float32; points with valid == 0

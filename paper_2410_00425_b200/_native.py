@@ -30,6 +30,7 @@ _F32 = ctypes.c_float
 _SIGNATURES = {
     "bs_abi_version": [],
     "bs_init": [_I32],
+    "bs_host_step": [_P, _P, _I64, _I32, _P, _P],
     "bs_quat_normalize_f64": [_P, _I64, _P, _P],
     "bs_quat_normalize_f32": [_P, _I64, _P, _P],
     "bs_pose_compose_f64": [_P, _P, _I64, _P, _P, _I64, _P, _P, _P],

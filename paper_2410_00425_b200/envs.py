@@ -22,7 +22,7 @@ import torch
 
 from . import _native as nat
 from . import cabi
-from .errors import DimensionError, InputError
+from .errors import BS_ERR_INPUT, DimensionError, InputError, raise_for_status
 
 
 @dataclass
@@ -285,7 +285,6 @@ class Env:
         if getattr(self, "_h_action", None) is None:
             self._h_action = torch.zeros((N, A), dtype=torch.float32).pin_memory()
             self._h_action_np = self._h_action.numpy()  # a view of the pinned buffer
-            self._h_zeros = np.zeros(N * A, dtype=np.float32)
             outs = self._host_outputs()
             # the arena's tensors come back in one copy; frames (render modes) one copy each
             self._h_arena = torch.zeros(self._out_arena.numel(), dtype=torch.uint8).pin_memory()
@@ -319,6 +318,11 @@ class Env:
         self._warm_launchers(lambda: self._launch_step(self.action_buf.data_ptr()))
         self._host_graph = self._capture(launch)
         self._host_graph_key = self._params_key()
+        self._host_graph_exec = self._host_graph.raw_cuda_graph_exec()
+        self._h_action_ptr = self._h_action.data_ptr()
+        self._dev_index = torch.device(self.device).index if torch.device(self.device).index is not None \
+            else torch.cuda.current_device()
+        self._lib = nat.load()
 
     def _arena_bytes(self) -> int:
         n = 0
@@ -363,18 +367,22 @@ class Env:
         call.  One graph launch and one stream synchronisation per step."""
         if self._host_graph is None:
             self.enable_host_io()
-        a = np.asarray(action, dtype=np.float32)
+        a = action
+        if not (type(a) is np.ndarray and a.dtype == np.float32 and a.flags.c_contiguous):
+            a = np.ascontiguousarray(action, dtype=np.float32)
         if a.shape != (self.num_envs, self.action_dim):
             raise DimensionError(f"action must have shape ({self.num_envs}, {self.action_dim}), got {a.shape}")
-        self._h_action_np[:, :self.action_dim] = a
-        # exact non-finite test in one BLAS pass: x * 0 is 0 for every finite x and NaN for
-        # inf / NaN, so the dot with zeros is finite iff every action is (no overflow possible)
-        if self.validate_actions and not np.isfinite(np.dot(self._h_action_np.reshape(-1), self._h_zeros)):
-            raise InputError("non-finite action")
         if self._host_graph_key != self._params_key():
             self.enable_host_io()
-        self._host_graph.replay()
-        torch.cuda.current_stream(self.device).synchronize()  # the stream replay() launched on
+        # one C call: stage the actions into the pinned buffer the graph reads (with the exact
+        # inf / NaN test, before anything is launched), replay the host-I/O graph on the current
+        # stream and wait for it
+        st = self._lib.bs_host_step(a.ctypes.data, self._h_action_ptr, a.size, int(self.validate_actions),
+                                    self._host_graph_exec, torch._C._cuda_getCurrentRawStream(self._dev_index))
+        if st:
+            if st == BS_ERR_INPUT:
+                raise InputError("non-finite action")
+            raise_for_status(st, "bs_host_step")
         return self._h_outs
 
     def host_io_bytes(self):

@@ -13,6 +13,7 @@ N = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 env = make_task("PickCube", N, seed=0)
 env.enable_host_io()
 acts = np.random.default_rng(0).uniform(-1, 1, (64, N, 3)).astype(np.float32)
+cold = np.random.default_rng(1).uniform(-1, 1, (400, N, 3)).astype(np.float32)  # bench-like: fresh rows
 
 
 def timeit(fn, n=400):
@@ -27,6 +28,7 @@ def timeit(fn, n=400):
 
 
 print(f"step_host (validated)      {timeit(lambda k: env.step_host(acts[k % 64])):7.1f} us")
+print(f"step_host (cold actions)   {timeit(lambda k: env.step_host(cold[k % 400])):7.1f} us")
 env.validate_actions = False
 print(f"step_host (no finite check){timeit(lambda k: env.step_host(acts[k % 64])):7.1f} us")
 stream = torch.cuda.current_stream()
@@ -39,3 +41,8 @@ for k in range(100):
 ev1.record()
 torch.cuda.synchronize()
 print(f"graph device time          {ev0.elapsed_time(ev1) * 10:7.1f} us")
+a = acts[0]
+print(f"python: shape+params key   {timeit(lambda k: (a.shape == (N, 3), env._params_key())):7.2f} us")
+print(f"python: raw stream         {timeit(lambda k: torch._C._cuda_getCurrentRawStream(0)):7.2f} us")
+print(f"python: current_stream    {timeit(lambda k: torch.cuda.current_stream(env.device).cuda_stream):7.2f} us")
+print(f"python: a.ctypes.data      {timeit(lambda k: a.ctypes.data):7.2f} us")
