@@ -52,7 +52,20 @@ __device__ long long g_bs_last;
   } while (0)
 // every CTA: its own duration (slots 22 max, 23 sum, 24 count) -- the launch is as long as its
 // slowest warp, not env 0's
-#define BS_CTA_BEGIN const long long bs_cta_t0_ = clock64()
+// and the launch window in globaltimer ns: slot 25 ~(earliest CTA entry) (a max of complements, so
+// the zero reset works), 27 latest CTA entry, 26 latest CTA exit
+__device__ __forceinline__ unsigned long long bs_gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define BS_CTA_BEGIN                                                           \
+  const long long bs_cta_t0_ = clock64();                                      \
+  if (threadIdx.x == 0) {                                                      \
+    const unsigned long long g_ = bs_gtimer();                                 \
+    atomicMax(&g_bs_phase[25], ~g_);                                           \
+    atomicMax(&g_bs_phase[27], g_);                                            \
+  }
 #define BS_CTA_END                                                             \
   do {                                                                         \
     if (threadIdx.x == 0) {                                                    \
@@ -60,6 +73,7 @@ __device__ long long g_bs_last;
       atomicMax(&g_bs_phase[22], d_);                                          \
       atomicAdd(&g_bs_phase[23], d_);                                          \
       atomicAdd(&g_bs_phase[24], 1ull);                                        \
+      atomicMax(&g_bs_phase[26], bs_gtimer());                                 \
     }                                                                          \
   } while (0)
 #else
@@ -1021,12 +1035,12 @@ __global__ void __launch_bounds__(32) k_step(const __grid_constant__ BsModelTabl
   const bool live = e_raw < S.num_envs;
   const int e = live ? e_raw : S.num_envs - 1;  // idle groups shadow the last env, never store
   R* E = smem + g * Y.total;
+  BS_CTA_BEGIN;
   const Model M = model_of(T, S.model_id[e]);
   // Am: the solver's actor block (smem staging, u, rows) = A_dyn; Ag: the actor stride of the
   // global state rows and of the obs layout = A_max (A_dyn <= A_max)
   const int Dm = K::EXACT ? MD : Y.Dm, Am = K::EXACT ? MA : Y.Am, Ag = K::EXACT ? MA : T.A_max;
   BS_TICK(0);
-  BS_CTA_BEGIN;
 
   // ---- stage the env's state rows
   #pragma unroll 1

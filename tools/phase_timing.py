@@ -67,6 +67,26 @@ def main():
         print(f"per-CTA duration over all launches: mean {mean_cta:.0f} cycles, max {buf[22]:.0f} cycles "
               f"({buf[22] / 1.965e3:.1f} us) -- the launch lasts as long as its slowest warp")
         out["cta_cycles_mean"], out["cta_cycles_max"] = mean_cta, buf[22]
+    # launch window: event-timed step kernel vs the CTAs' globaltimer span (entry of the first CTA
+    # to exit of the last), one launch at a time
+    win = []
+    for k in range(20):
+        nat.call("bs_debug_phase_clocks", ctypes.addressof(buf), 32, 1)  # reset
+        env.random_actions(1000 + k)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        env.launch_step()
+        e1.record()
+        torch.cuda.synchronize()
+        nat.call("bs_debug_phase_clocks", ctypes.addressof(buf), 32, 0)
+        first = (~buf[25]) & ((1 << 64) - 1)
+        win.append((e0.elapsed_time(e1) * 1e3, (buf[26] - first) / 1e3, (buf[27] - first) / 1e3))
+    ev = sorted(w[0] for w in win)[len(win) // 2]
+    span = sorted(w[1] for w in win)[len(win) // 2]
+    ramp = sorted(w[2] for w in win)[len(win) // 2]
+    print(f"launch window (median of 20): event-timed step {ev:.1f} us, CTA span (first entry -> last exit) "
+          f"{span:.1f} us, CTA entry ramp {ramp:.1f} us")
+    out["launch_window_us"] = {"event": ev, "cta_span": span, "entry_ramp": ramp}
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", "phase_timing.json"), "w") as f:
         json.dump(out, f, indent=1)
