@@ -31,6 +31,8 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC",
           "-I" + os.path.join(ROOT, "include")]
 if os.environ.get("BS_PHASE_TIMING"):  # developer instrumentation build (tools/phase_timing.py)
     COMMON.append("-DBS_PHASE_TIMING")
+if os.environ.get("BS_EXTRA_NVCC"):  # developer A/B variants (tools/gpu_lib_ab.sh), e.g. -DBS_NO_L2_PREFETCH
+    COMMON.extend(os.environ["BS_EXTRA_NVCC"].split())
 # Per-file extra flags.  NOFMA: numpy-order arithmetic must not be contracted.
 NOFMA = ["-fmad=false"]
 SOURCES = {

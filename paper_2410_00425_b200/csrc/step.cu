@@ -294,15 +294,15 @@ __device__ __forceinline__ int narrow_pair(const Model& M, int pi, const R* spq,
       depth = sa[0] - dist;
     } else {
       int kk = 0;
-      R best = h[0] - fabs(l3[0]);
+      R best = h[0] - fabs(l3[0]), lk = l3[0], hk = h[0];  // selects, not indexed arrays (no local memory)
 #pragma unroll
       for (int k = 1; k < 3; ++k) {
         R pen = h[k] - fabs(l3[k]);
-        if (pen < best) { best = pen; kk = k; }
+        if (pen < best) { best = pen; kk = k; lk = l3[k]; hk = h[k]; }
       }
-      R sg = l3[kk] >= 0.0 ? 1.0 : -1.0;
+      R sg = lk >= 0.0 ? 1.0 : -1.0;
 #pragma unroll
-      for (int k = 0; k < 3; ++k) { nl[k] = k == kk ? sg : 0.0; sl[k] = k == kk ? sg * h[kk] : l3[k]; }
+      for (int k = 0; k < 3; ++k) { nl[k] = k == kk ? sg : 0.0; sl[k] = k == kk ? sg * hk : l3[k]; }
       depth = sa[0] + best;
     }
     V3<R> n = quat_rotate(qb, v3(nl[0], nl[1], nl[2]));
@@ -684,10 +684,10 @@ __device__ __forceinline__ void substep(const Model& M, const BsSimParams& P, co
     const int pi = (int)cc[7];
     V3<R> dir;
     {  // tangent basis (A-6): t1 = normalize(n x e_k), e_k the least-aligned axis; t2 = n x t1
-      const R an[3] = {fabs(n.x), fabs(n.y), fabs(n.z)};
-      int k = 0;
-      if (an[1] < an[k]) k = 1;
-      if (an[2] < an[k]) k = 2;
+      int k = 0;  // (selects, not an indexed array: no local-memory round trip per row)
+      R amin = fabs(n.x);
+      if (fabs(n.y) < amin) { k = 1; amin = fabs(n.y); }
+      if (fabs(n.z) < amin) k = 2;
       V3<R> t1 = crs(n, v3(k == 0, k == 1, k == 2));
       t1 = scl(t1, rsqrt(dot(t1, t1)));
       dir = t == 0 ? n : (t == 1 ? t1 : crs(n, t1));
@@ -1037,6 +1037,12 @@ __global__ void __launch_bounds__(32) k_step(const __grid_constant__ BsModelTabl
   R* E = smem + g * Y.total;
   BS_CTA_BEGIN;
   const Model M = model_of(T, S.model_id[e]);
+  // the env's scalar state is read here, at entry, so its (cold-L2) misses overlap the staging
+  // instead of stalling the epilogue
+  const bool div_in = S.diverged[e] != 0;
+  const int32_t el_in = S.elapsed[e], tdof_in = S.target_dof[e];
+  const double ret_in = S.ep_return ? S.ep_return[e] : 0.0;
+  const uint8_t epf_in = S.ep_return ? S.ep_flags[e] : 0;
   // Am: the solver's actor block (smem staging, u, rows) = A_dyn; Ag: the actor stride of the
   // global state rows and of the obs layout = A_max (A_dyn <= A_max)
   const int Dm = K::EXACT ? MD : Y.Dm, Am = K::EXACT ? MA : Y.Am, Ag = K::EXACT ? MA : T.A_max;
@@ -1104,7 +1110,7 @@ __global__ void __launch_bounds__(32) k_step(const __grid_constant__ BsModelTabl
       E[Y.tgtv + i] = tgtv;
     }
   }
-  bool diverged = S.diverged[e] != 0;
+  bool diverged = div_in;
   __syncwarp();
   BS_TICK(1);
 
@@ -1134,7 +1140,7 @@ __global__ void __launch_bounds__(32) k_step(const __grid_constant__ BsModelTabl
   const R* lpq = E + Y.lpq;
   float reward = 0.0f;
   bool success = false, fail = diverged;
-  int32_t tdof = S.target_dof[e];
+  int32_t tdof = tdof_in;
   if (P.task == BS_TASK_PICKCUBE) {
     const R* f = P.task_f;
     const V3<R> ee = ld3(lpq + 7 * P.ee_link);
@@ -1156,7 +1162,7 @@ __global__ void __launch_bounds__(32) k_step(const __grid_constant__ BsModelTabl
     fail = fabs(th) > P.task_f[3] || fabs(x) > P.task_f[4] || diverged;
     reward = (float)cos(th);
   }
-  int32_t el = S.elapsed[e] + 1;
+  int32_t el = el_in + 1;
   const bool terminated = P.early_termination ? (success || fail) : false;
   const bool truncated = el >= P.max_steps;
   if (live && l == 0) {
@@ -1170,8 +1176,8 @@ __global__ void __launch_bounds__(32) k_step(const __grid_constant__ BsModelTabl
     // EpisodeMetrics: return = sum of rewards, *_once latch, *_at_end
     // sampled at the final step; emitted when the episode ends, accumulators restart.
     if (S.ep_return) {
-      const double ret = S.ep_return[e] + (double)reward;
-      const uint8_t fl = S.ep_flags[e] | (success ? 1 : 0) | (fail ? 2 : 0);
+      const double ret = ret_in + (double)reward;
+      const uint8_t fl = epf_in | (success ? 1 : 0) | (fail ? 2 : 0);
       const bool ended = terminated || truncated;
       if (O.ep_done) {
         O.ep_done[e] = ended;
@@ -1192,6 +1198,7 @@ __global__ void __launch_bounds__(32) k_step(const __grid_constant__ BsModelTabl
   if (done && O.final_obs) pack_state_obs<G>(M, P, Y, E, O.final_obs + (int64_t)e * O.obs_dim, O.obs_dim, Dm, Ag, l);
   uint8_t div_out = diverged;
   if (__any_sync(FULLMASK, done)) {
+    __syncwarp();  // the group's final_obs reads of E above precede lane 0's reset writes (WAR)
     if (done && l == 0) {
       const uint32_t rc = (uint32_t)S.reset_count[e] + 1u;
       S.reset_count[e] = rc;
