@@ -156,6 +156,35 @@ def _traffic(kernel: str, workload: str):
         return None
 
 
+def _issue(kernel: str, workload: str, units: int, launch_s: float, sm_mhz):
+    """The instruction-issue side of the roofline (the kernels are latency / issue bound, not
+    HBM bound): warp instructions per launch from the committed ncu counters
+    (profiles/issue.json, tools/ncu_issue.py; scaled to this launch's env / frame count) over the
+    issue capacity of the launch measured here, 4 SMSPs x SMs x SM clock x launch time; plus the
+    fp64 FLOP rate (thread-level DFMA x 2 + DADD + DMUL, replicated lanes included) against the
+    fp64 pipe's 64 DFMA / SM / clock.  None without a capture for this workload."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "issue.json")) as f:
+            doc = json.load(f)
+        rec = (doc.get(workload) or doc[workload.split("_")[0]])[kernel]  # c3_4096: the c3 counts, scaled
+    except (OSError, ValueError, KeyError):
+        return None
+    import torch
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    hz = (sm_mhz or 1965.0) * 1e6
+    scale = units / rec["units"]
+    inst = rec["warp_inst"] * scale
+    flop = (2 * rec["fp64_dfma_thread_ops"] + rec["fp64_dadd_thread_ops"] + rec["fp64_dmul_thread_ops"]) * scale
+    slots = 4 * sms * hz * launch_s
+    fp64_peak = 64 * 2 * sms * hz
+    return {"warp_inst_per_launch": inst, "issue_slots_per_launch": slots, "frac": inst / slots,
+            "fp64_tflops": flop / launch_s / 1e12, "fp64_peak_tflops": fp64_peak / 1e12,
+            "fp64_frac": flop / launch_s / fp64_peak,
+            "ncu_issue_active": rec["ncu_issue_active"], "ncu_fp64_pipe_active": rec["ncu_fp64_pipe_active"],
+            "source": "warp-instruction and fp64 thread-op counts per launch from ncu (" + rec["_capture"] +
+                      ", scaled by units); launch time measured here; SM clock = the sampled median"}
+
+
 def sim_bytes_per_env_step(scene, obs_dim, action_dim):
     """Algorithmic bytes of one env-step on SURVEY.md section 8(d)'s basis:
     the action read; articulation (qpos, qvel) and actor (pose 7 + vel 6) state read + write;
@@ -528,10 +557,13 @@ def run_workload(name, steps, warmup, world, rank, local, dist, flush, seed, e2e
         if rs > sim_s:
             dominant = "k_render"
     dk = kernels[dominant]
+    sm_mhz = m["clocks"].get("sm_mhz")
+    for k, v in kernels.items():
+        v["issue"] = _issue(k, name, N, v["us_per_launch"] / 1e6, sm_mhz)
     roof = {"bound": "hbm", "achieved": dk["achieved_gbs"], "peak": peak, "unit": "GB/s",
             "frac": dk["achieved_gbs"] / peak, "traffic": _traffic(dominant, name), "kernel": dominant,
             "bytes_per_env_step": dk["bytes_per_env_step"], "kernel_us_per_launch": dk["us_per_launch"],
-            "peak_source": peak_kind, "kernels": kernels}
+            "peak_source": peak_kind, "issue": dk["issue"], "kernels": kernels}
     line = {"metric": METRIC, "value": value, "unit": "env-steps/s", "n_gpus": world, "steps": steps,
             "warmup": warmup, "ms_per_step": m["step_ms"] / steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",

@@ -20,6 +20,11 @@ BENCH_DIST_BACKEND=gloo timeout 300 python -m torch.distributed.run --nnodes=1 -
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 5 --warmup 3 --no-cpu --secondary c3 > /dev/null 2>> gpurun_out/${TAG}_ncu.err
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_step -s 3 -c 1 -o gpurun_out/${TAG}_prof_step python bench.py --steps 3 --warmup 3 --no-cpu --secondary "" > /dev/null 2>> gpurun_out/${TAG}_ncu.err
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_render -s 3 -c 1 -o gpurun_out/${TAG}_prof_render python bench.py --config c3 --steps 3 --warmup 3 --no-cpu --secondary "" > /dev/null 2>> gpurun_out/${TAG}_ncu.err
+# issue / fp64 counters of the render kernel on C4 and C5 (tools/ncu_issue.py -> profiles/issue.json)
+M=smsp__inst_executed.sum,smsp__cycles_elapsed.avg,gpu__time_duration.sum,smsp__issue_active.avg.pct_of_peak_sustained_active,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,smsp__sass_thread_inst_executed_op_dfma_pred_on.sum.per_cycle_elapsed,smsp__sass_thread_inst_executed_op_dadd_pred_on.sum.per_cycle_elapsed,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum.per_cycle_elapsed
+for c in c4 c5; do
+  timeout 600 ncu --metrics $M --clock-control none -k regex:k_render -s 3 -c 1 -o gpurun_out/${TAG}_issue_render_$c python bench.py --config $c --steps 3 --warmup 3 --no-cpu --secondary "" > /dev/null 2>> gpurun_out/${TAG}_ncu.err
+done
 if [ "$3" == "phase" ]; then
   timeout 600 python tools/phase_timing.py 4096 50 > gpurun_out/${TAG}_phase.txt 2>&1
 fi
