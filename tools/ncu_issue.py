@@ -26,7 +26,8 @@ def raw(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], check=True, capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    return [dict(zip(rows[0], r)) for r in rows[2:]]
+    units = dict(zip(rows[0], rows[1]))
+    return [dict(zip(rows[0], r)) for r in rows[2:]], units
 
 
 def main():
@@ -36,7 +37,9 @@ def main():
     for arg in sys.argv[1:]:
         wl, spec = arg.split("=", 1)
         rep, units = spec.rsplit(":", 1)
-        for r in raw(rep):
+        recs, unit = raw(rep)
+        to_us = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3, "s": 1e6, "second": 1e6}[unit["gpu__time_duration.sum"]]
+        for r in recs:
             name = r["Kernel Name"].split("(")[0].split("<")[0].replace("void ", "").strip()
             cyc = float(r["smsp__cycles_elapsed.avg"])
             f = lambda k: float(r[k].replace(",", "")) * cyc  # noqa: E731 (per-cycle sums -> per launch)
@@ -48,9 +51,8 @@ def main():
                 "fp64_dmul_thread_ops": int(f("smsp__sass_thread_inst_executed_op_dmul_pred_on.sum.per_cycle_elapsed")),
                 "ncu_issue_active": float(r["smsp__issue_active.avg.pct_of_peak_sustained_active"]) / 100,
                 "ncu_fp64_pipe_active": float(r["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"]) / 100,
-                "ncu_us": float(r["gpu__time_duration.sum"]) / 1e3 if float(r["gpu__time_duration.sum"]) > 1e4
-                else float(r["gpu__time_duration.sum"]),
-                "_capture": os.path.relpath(rep, ROOT),
+                "ncu_us": float(r["gpu__time_duration.sum"].replace(",", "")) * to_us,
+                "_capture": os.path.basename(rep) + " (tools/gpu_round.sh)",
             }
     with open(path, "w") as fh:
         json.dump(doc, fh, indent=1)
