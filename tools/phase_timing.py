@@ -46,7 +46,11 @@ def main():
     torch.cuda.synchronize()
     buf = (ctypes.c_ulonglong * 32)()
     nat.call("bs_debug_phase_clocks", ctypes.addressof(buf), 32, 1)  # reset
+    # PHASE_FLUSH=1: a 256 MiB write before every timed step (cold L2, as in bench.py)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if os.environ.get("PHASE_FLUSH") else None
     for k in range(steps):
+        if flush is not None:
+            flush.zero_()
         env.step_random(100 + k)
     torch.cuda.synchronize()
     nat.call("bs_debug_phase_clocks", ctypes.addressof(buf), 32, 0)
