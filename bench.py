@@ -185,6 +185,36 @@ def _issue(kernel: str, workload: str, units: int, launch_s: float, sm_mhz):
                       ", scaled by units); launch time measured here; SM clock = the sampled median"}
 
 
+_PCIE = {}
+
+
+def pcie_peak_gbs(local: int) -> dict:
+    """Measured host<->device copy-engine bandwidth of this box (pinned host memory, 256 MiB,
+    best of 5, CUDA events; once per process): the roofline of the `e2e` path, whose per-step
+    bytes cross PCIe."""
+    if local in _PCIE:
+        return _PCIE[local]
+    import torch
+    dev = torch.device("cuda", local)
+    n = 256 << 20
+    h = torch.empty(n, dtype=torch.uint8).pin_memory()
+    d = torch.empty(n, dtype=torch.uint8, device=dev)
+    out = {}
+    for name, (dst, src) in (("d2h", (h, d)), ("h2d", (d, h))):
+        best = 0.0
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dst.copy_(src, non_blocking=True)
+            e1.record()
+            torch.cuda.synchronize()
+            best = max(best, n / (e0.elapsed_time(e1) / 1e3) / 1e9)
+        out[name] = best
+    del h, d
+    _PCIE[local] = out
+    return out
+
+
 def sim_bytes_per_env_step(scene, obs_dim, action_dim):
     """Algorithmic bytes of one env-step on SURVEY.md section 8(d)'s basis:
     the action read; articulation (qpos, qvel) and actor (pose 7 + vel 6) state read + write;
@@ -538,7 +568,16 @@ def run_workload(name, steps, warmup, world, rank, local, dist, flush, seed, e2e
     stats = torch.stack([env.success.sum().double(), env.terminated.sum().double(), env.truncated.sum().double()])
     bdist.reduce_stats(stats)  # rollout statistics: the only data collective
     e2e_s, h2d, d2h = measure_e2e(env, e2e_steps, dist, seed + rank)
-    e2e = {"value": n_global * e2e_steps / e2e_s, "unit": "env-steps/s", "h2d_bytes_per_step": h2d,
+    pcie = pcie_peak_gbs(local)
+    # the e2e path's own roofline: its per-step host<->device bytes over the measured copy-engine
+    # bandwidth (the bytes of one step cross PCIe in sequence: actions in, results out)
+    io_gbs = (h2d + d2h) * (e2e_steps / e2e_s) / 1e9
+    io_peak = 1.0 / (h2d / (pcie["h2d"] * 1e9) + d2h / (pcie["d2h"] * 1e9)) * (h2d + d2h) / 1e9 if h2d + d2h else None
+    e2e_roof = {"bound": "pcie", "achieved": io_gbs, "peak": io_peak, "unit": "GB/s",
+                "frac": io_gbs / io_peak if io_peak else None, "pcie_measured_gbs": pcie,
+                "source": "h2d/d2h bytes per step x steps/s over the measured pinned copy bandwidth"}
+    e2e = {"value": n_global * e2e_steps / e2e_s, "unit": "env-steps/s", "roofline": e2e_roof,
+           "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h, "steps": e2e_steps,
            "path": "Env.step_host: one CUDA graph per step = step kernel reading the pinned host actions and "
                    "writing obs/reward/flags to pinned host memory over PCIe (zero-copy) (+ render + D2H of "
