@@ -295,7 +295,8 @@ typedef struct BsRenderParams {
   double light_dir[3];         /* unit vector towards the light, world frame */
   float ambient, diffuse;      /* flat shading: ambient + diffuse * max(0, n.l) (A-12) */
   float background[3];         /* rgb in [0,1] of empty pixels */
-  int32_t tile;                /* CTA tile edge in pixels (0 = default 128) */
+  int32_t tile;                /* tile size: a CTA's key buffer holds tile^2 pixels, laid out as a
+                                  full-width strip up to 256 pixels wide (0 = default 128) */
   float* frame_scratch;        /* optional device scratch [N][C][12 S_max + 20] floats: per-frame
                                   shape -> camera transforms and camera block, computed by a
                                   parallel pre-pass (NULL: computed inside the rasterizer) */

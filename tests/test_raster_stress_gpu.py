@@ -62,7 +62,8 @@ def _random_views(rng, n):
     return out
 
 
-@pytest.mark.parametrize("res,obs_mode", [((128, 128), "rgbd"), ((97, 61), "rgbd"), ((200, 150), "pointcloud")])
+@pytest.mark.parametrize("res,obs_mode", [((128, 128), "rgbd"), ((97, 61), "rgbd"), ((200, 150), "pointcloud"),
+                                          ((300, 90), "rgbd")])
 def test_random_views_all_tiles_bit_exact(cuda, res, obs_mode):
     from paper_2410_00425_b200.cameras import CameraConfig, pinhole
     from paper_2410_00425_b200.tasks import make_task
