@@ -148,6 +148,36 @@ class Renderer:
                      ctypes.byref(self.mesh.c), ctypes.byref(g["c_cams"]), ecp, ctypes.byref(self.c_params),
                      ctypes.byref(g["c_out"]), nat.stream_handle())
 
+    def render_chunks(self, scene, nchunks, after_chunk):
+        """Render every camera group in `nchunks` launches over contiguous env ranges, calling
+        `after_chunk(a, b)` after each chunk's launch (same stream) -- the host-I/O step starts a
+        chunk's frame copies while the next chunk renders.  Frames are identical to `render`'s
+        (every frame is independent; the pre-pass scratch and frame queue are reused in stream
+        order)."""
+        N = scene.num_envs
+        bounds = [N * i // nchunks for i in range(nchunks + 1)]
+        for i in range(nchunks):
+            a, b = bounds[i], bounds[i + 1]
+            if a == b:
+                continue
+            cs = scene.c_state_slice(a, b)
+            ecp = self.env_color[a:].data_ptr() if self.env_color is not None else None
+            for g in self.groups:
+                cb = cabi.BsCameraBatch.from_buffer_copy(g["c_cams"])
+                cb.pose, cb.intrinsics = g["pose"][a:].data_ptr(), g["intr"][a:].data_ptr()
+                fb = cabi.BsFrameBatch()
+                fb.rgb, fb.depth, fb.seg = g["rgb"][a:].data_ptr(), g["depth"][a:].data_ptr(), g["seg"][a:].data_ptr()
+                fb.pointcloud = g["pc"][a:].data_ptr() if g["pc"] is not None else None
+                nat.call("bs_render", ctypes.byref(scene.c_tables), ctypes.byref(cs), ctypes.byref(self.mesh.c),
+                         ctypes.byref(cb), ecp, ctypes.byref(self.c_params), ctypes.byref(fb), nat.stream_handle())
+            after_chunk(a, b)
+
+    def buffer_storages(self):
+        """Storage pointers of the frame buffers (an observation tensor that is a view of one of
+        them can be copied env-chunk by env-chunk)."""
+        return {t.untyped_storage().data_ptr() for g in self.groups
+                for t in (g["rgb"], g["depth"], g["seg"], g["pc"]) if t is not None}
+
     def frames(self):
         """{camera name: {"rgb", "depth", "seg"[, "pointcloud"]}} views of the device buffers."""
         out = {}

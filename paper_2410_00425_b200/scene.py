@@ -339,6 +339,16 @@ class SceneBatch:
             setattr(cs, k, getattr(self, k).data_ptr())
         self.c_state = cs
 
+    def c_state_slice(self, a: int, b: int):
+        """The C state struct of envs [a, b) (pointers into the same rows; env_offset shifted so
+        global env indices -- RNG keys -- stay the same)."""
+        cs = cabi.BsEnvState()
+        cs.num_envs, cs.env_offset = b - a, self.env_offset + a
+        for k in ("model_id", "qpos", "qvel", "target", "actor_pose", "actor_vel", "link_pose", "goal",
+                  "diverged", "elapsed", "reset_count", "target_dof", "ep_return", "ep_flags"):
+            setattr(cs, k, getattr(self, k)[a:].data_ptr())
+        return cs
+
     STATE_FIELDS = ("qpos", "qvel", "target", "actor_pose", "actor_vel", "link_pose", "goal", "diverged",
                     "elapsed", "reset_count", "target_dof", "ep_return", "ep_flags")
 
