@@ -107,9 +107,11 @@ struct Lay {
 
 // EX_ = the launch guarantees D_max == MD and A_max == MA exactly, so the padded widths
 // (D_max, A_max, NU and the row stride) are compile-time constants in the kernel.
-template <int G_, int MD_, int MA_, bool EX_ = false, int SLOT_ = 1>
+// SA_ = the free actors the solver carries (NU = MD + 6 SA); 0 for scenes without free actors
+// (cabinets: A_max is padded to 1 but A_dyn = 0), whose u then fits the register-resident sweep.
+template <int G_, int MD_, int MA_, bool EX_ = false, int SLOT_ = 1, int SA_ = MA_>
 struct Cfg {
-  static constexpr int G = G_, MD = MD_, MA = MA_, EPW = 32 / G_, NU = MD_ + 6 * MA_;
+  static constexpr int G = G_, MD = MD_, MA = MA_, EPW = 32 / G_, NU = MD_ + 6 * SA_;
   static constexpr bool EXACT = EX_;
   static constexpr int SLOT = SLOT_;  // bs::LaunchCache slot of this variant's smem opt-in
 };
@@ -1358,6 +1360,9 @@ typedef Cfg<8, 12, 1, false, 3> CfgArt;     // articulated objects (arm + cabine
 typedef Cfg<16, 12, 1, false, 7> CfgArt16;
 typedef Cfg<32, 12, 1, false, 8> CfgArt32;
 typedef Cfg<8, 12, 4, false, 4> CfgLarge;   // general scenes: D <= 12, <= 4 actors
+typedef Cfg<8, 12, 1, false, 9, 0> CfgArt0;     // articulated objects without free actors (A_dyn = 0)
+typedef Cfg<16, 12, 1, false, 10, 0> CfgArt0_16;
+typedef Cfg<32, 12, 1, false, 11, 0> CfgArt0_32;
 
 }  // namespace step
 }  // namespace bs
@@ -1416,6 +1421,12 @@ int bs_step(const BsModelTables* T, const BsEnvState* S, const BsStepOutputs* O,
     return launch<CfgPick>(*T, *S, *O, *P, action, st);
   }
   if (T->D_max <= CfgSmall::MD && T->A_max <= CfgSmall::MA) return launch<CfgSmall>(*T, *S, *O, *P, action, st);
+  if (T->D_max <= CfgArt0::MD && T->A_max <= CfgArt0::MA && T->A_dyn == 0) {
+    const int g = lanes(S->num_envs);
+    if (g == 32) return launch<CfgArt0_32>(*T, *S, *O, *P, action, st);
+    if (g == 16) return launch<CfgArt0_16>(*T, *S, *O, *P, action, st);
+    return launch<CfgArt0>(*T, *S, *O, *P, action, st);
+  }
   if (T->D_max <= CfgArt::MD && T->A_max <= CfgArt::MA) {
     const int g = lanes(S->num_envs);
     if (g == 32) return launch<CfgArt32>(*T, *S, *O, *P, action, st);
