@@ -1409,26 +1409,29 @@ int bs_step(const BsModelTables* T, const BsEnvState* S, const BsStepOutputs* O,
     const int g = v ? atoi(v) : 0;
     return g == 8 || g == 16 || g == 32 ? g : 0;
   }();
-  auto lanes = [&](int n) {
+  // per_sm: env-lanes per SM per launch that keep the step one short wave; measured per family
+  // (same box, BS_STEP_G): PickCube-style 1024 envs G 8 / 16 / 32 = 66.0 / 62.9 / 60.1 us (224 ->
+  // G 32), cabinets 115.2 / 96.0 / 100.7 us (112 -> G 16)
+  auto lanes = [&](int n, long per_sm) {
     if (gforce) return gforce;
-    const long budget = 112L * bs::sm_count();  // env-lanes per launch that keep the step one short wave
+    const long budget = per_sm * bs::sm_count();
     return (long)n * 32 <= budget ? 32 : ((long)n * 16 <= budget ? 16 : 8);
   };
   if (!generic && T->D_max == CfgPick::MD && T->A_max == CfgPick::MA && T->A_dyn == CfgPick::MA) {
-    const int g = lanes(S->num_envs);
+    const int g = lanes(S->num_envs, 224);
     if (g == 32) return launch<CfgPick32>(*T, *S, *O, *P, action, st);
     if (g == 16) return launch<CfgPick16>(*T, *S, *O, *P, action, st);
     return launch<CfgPick>(*T, *S, *O, *P, action, st);
   }
   if (T->D_max <= CfgSmall::MD && T->A_max <= CfgSmall::MA) return launch<CfgSmall>(*T, *S, *O, *P, action, st);
   if (T->D_max <= CfgArt0::MD && T->A_max <= CfgArt0::MA && T->A_dyn == 0) {
-    const int g = lanes(S->num_envs);
+    const int g = lanes(S->num_envs, 112);
     if (g == 32) return launch<CfgArt0_32>(*T, *S, *O, *P, action, st);
     if (g == 16) return launch<CfgArt0_16>(*T, *S, *O, *P, action, st);
     return launch<CfgArt0>(*T, *S, *O, *P, action, st);
   }
   if (T->D_max <= CfgArt::MD && T->A_max <= CfgArt::MA) {
-    const int g = lanes(S->num_envs);
+    const int g = lanes(S->num_envs, 112);
     if (g == 32) return launch<CfgArt32>(*T, *S, *O, *P, action, st);
     if (g == 16) return launch<CfgArt16>(*T, *S, *O, *P, action, st);
     return launch<CfgArt>(*T, *S, *O, *P, action, st);
