@@ -52,6 +52,14 @@ def test_our_arm_contract(cuda):
     c = d["clocks"]
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(c)
     assert d["e2e"]["h2d_bytes_per_step"] == 256 * 3 * 4 and d["e2e"]["d2h_bytes_per_step"] > 0
+    # the e2e path's own roofline: host<->device bytes per second over the measured PCIe copy rate
+    er = d["e2e"]["roofline"]
+    assert er["bound"] == "pcie" and er["peak"] > 1.0 and 0 < er["frac"] <= 1.5
+    assert er["pcie_measured_gbs"]["d2h"] > 1.0 and er["pcie_measured_gbs"]["h2d"] > 1.0
+    # the issue side of the roofline (ncu counts in profiles/issue.json, scaled to this launch)
+    iss = r["issue"]
+    assert iss is not None and 0 < iss["frac"] < 1 and 0 < iss["fp64_frac"] < 1
+    assert iss["issue_slots_per_launch"] > iss["warp_inst_per_launch"] > 0
 
 
 @pytest.mark.parametrize("config", ["c4", "c5"])
